@@ -1,0 +1,426 @@
+"""Benchmark of the RTCG hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Headline workload (BASELINE.json configs[1]): ``ReductionKernel`` dot product
+``sum(x*y)``, float32, n = 2^28 elements per GPU (weak scaling), block/unroll
+autotuned before the timed region.  One step = one full reduction of the
+resident inputs (per-CTA folds + in-kernel ordered combine; for N > 1 also the
+NCCL all-gather of the per-rank partials and the rank-ordered combine).
+``value`` = algorithmic bytes (8 B/element: x and y read once) of all ranks /
+max-over-ranks device time.  Inputs (2 x 1 GiB per GPU) exceed the 126 MB L2,
+so no flush is needed between steps.
+
+The JSON line also carries: ``e2e`` (same metric through the public API with
+pinned host inputs copied in and the scalar read back every step),
+``roofline`` (dominant kernel vs MEASURED_PEAKS.json HBM copy bandwidth),
+``cpu_baseline`` (the reference's CPU kernel on this host, bounded sample),
+``clocks`` (NVML during the timed region) and ``workloads`` (the other
+configs measured the same way: axpy, f64 poly+sin, max|x|, L2, int64 sum).
+
+``--impl reference`` times the reference's own CPU implementation of the same
+workload (``oracle/_ref``: C emitted by rtcg-kit's generator, compiled with its
+command line, driven with its threading) on all host cores of rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_PER_GPU = 1 << 28
+METRIC = "Elementwise/reduction GB/s vs B200 HBM peak at 1/2/4/8 GPU; speedup vs CPU ref"
+WORKLOAD = "ReductionKernel dot sum(x*y) float32 n=2^28 per GPU, autotuned block/unroll"
+FALLBACK_HBM = 6650.0
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    path = ROOT / "MEASURED_PEAKS.json"
+    if path.exists():
+        data = json.loads(path.read_text())
+        return float(data["hbm_gbs"]), "measured"
+    return FALLBACK_HBM, "fallback"
+
+
+# --- clocks ------------------------------------------------------------------------------------
+
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons while running."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period: float = 0.02) -> None:
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover - no NVML
+            self._nv = None
+            self.error = str(exc)
+
+    def _sample(self):
+        nv = self._nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        for bit, name in self.REASONS.items():
+            if mask & bit:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self._period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._sample()
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def summary(self) -> dict:
+        if self._nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.error}
+        busy = [s for s in self.samples if s > 0]
+        return {"sm_mhz": float(np.median(busy)) if busy else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons - {"gpu_idle"}),
+                "samples": len(self.samples)}
+
+
+# --- distributed plumbing ------------------------------------------------------------------------
+
+
+class Dist:
+    def __init__(self, gpus: int) -> None:
+        self.world = _env_int("WORLD_SIZE", 1)
+        self.rank = _env_int("RANK", 0)
+        self.local = _env_int("LOCAL_RANK", 0)
+        if self.world != gpus and "WORLD_SIZE" in os.environ:
+            print(f"warning: --gpus {gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
+        self.torch = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, value: float) -> float:
+        if self.world == 1:
+            return value
+        t = self.torch.tensor([value], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# --- CPU reference ---------------------------------------------------------------------------------
+
+
+def cpu_reference(workload: str, budget_s: float = 12.0, n_sample: int = 1 << 26):
+    """Time the reference CPU kernel on a bounded sample; returns a dict."""
+    from oracle import refdrive
+    fn, kind = refdrive.load(workload)
+    threads = refdrive.host_threads()
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, n_sample).astype(np.float32)
+    y = rng.uniform(-1, 1, n_sample).astype(np.float32)
+    fn(x, y, workers=threads)  # warm (page in, thread spin-up)
+    times, t_end = [], time.perf_counter() + budget_s
+    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
+        t0 = time.perf_counter()
+        fn(x, y, workers=threads)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": round(8 * n_sample / best / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": kind, "seconds_per_call": best, "calls": len(times),
+            "sample": f"dot f32 n=2^{int(math.log2(n_sample))} (of the 2^28 workload), "
+                      f"x,y~U(-1,1) seed 0, reference variant unroll=4 contiguous, "
+                      f"{threads} worker threads, best of {len(times)} calls"}
+
+
+def run_reference(args) -> int:
+    d = Dist(args.gpus)
+    if d.rank != 0:
+        d.close()
+        return 0
+    base = cpu_reference("dot_k", budget_s=max(3.0, 0.5 * args.steps))
+    line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": base["calls"], "warmup": 1,
+            "ms_per_step": round(base["seconds_per_call"] * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": WORKLOAD + " (CPU: bounded sample)",
+                                            "n": 1 << 26},
+            "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    d.close()
+    return 0
+
+
+# --- GPU arm ----------------------------------------------------------------------------------------
+
+
+def _time_steps(rt, step, k: int):
+    """Device time of k steps on the current stream, plus per-step durations."""
+    events = [rt.Event() for _ in range(k + 1)]
+    events[0].record()
+    for j in range(k):
+        step()
+        events[j + 1].record()
+    events[-1].synchronize()
+    per = [events[j].elapsed_ms(events[j + 1]) for j in range(k)]
+    return events[0].elapsed_ms(events[-1]), per
+
+
+def run_ours(args) -> int:
+    d = Dist(args.gpus)
+    from paper_0911_3456_b200 import _runtime as rt
+    from paper_0911_3456_b200 import autotune as at
+    from paper_0911_3456_b200 import ndarray as nd
+    from paper_0911_3456_b200 import parallel as par
+    from paper_0911_3456_b200 import reduction as rd
+    from paper_0911_3456_b200 import elementwise as ew
+
+    rt.set_device(d.local)
+    info = rt.device_info(d.local)
+    stream_handle = d.torch.cuda.current_stream().cuda_stream if d.world > 1 else 0
+    pool = nd.MemoryPool(device=d.local)
+    n = N_PER_GPU
+    total_n = n * d.world
+    peak, peak_kind = _peaks()
+
+    with rt.use_stream(stream_handle):
+        # resident inputs: this rank's slice of a global 2^28*N array
+        lo, _ = par.shard_range(total_n, d.rank, d.world)
+        hx = nd.pinned_empty((n,), nd.float32)
+        hy = nd.pinned_empty((n,), nd.float32)
+        rng = np.random.default_rng([0, d.rank])
+        hx[:] = rng.uniform(-1, 1, n).astype(np.float32)
+        hy[:] = rng.uniform(-1, 1, n).astype(np.float32)
+        gx, gy = nd.from_host(pool, nd.float32, hx), nd.from_host(pool, nd.float32, hy)
+        sx = par.ShardedArray(gx, lo, total_n, d.rank, d.world)
+        sy = par.ShardedArray(gy, lo, total_n, d.rank, d.world)
+
+        # autotune block x unroll for (dot, float32, n) -- outside the timed region
+        spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
+        t0 = time.perf_counter()
+        tuned = at.tune_reduction(spec, "dot_k", n, {"unroll": (1, 2, 4, 8),
+                                                     "block": (128, 256, 512, 1024)},
+                                  args=[gx, gy],
+                                  protocol=at.MeasurementProtocol(warmup=2, repeats=5),
+                                  store=at.TuneStore())
+        tune_s = time.perf_counter() - t0
+        best = tuned.best_assignment
+        kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
+        out = pool.alloc_uninitialized(nd.float32, ())
+
+        if d.world == 1:
+            def step():
+                kernel.launch(gx, gy, out=out)
+        else:
+            def step():
+                par.sharded_reduce(kernel, sx, sy, return_device=True).free()
+
+        # correctness of the tuned kernel on this data (cheap, before timing)
+        value = kernel(gx, gy)
+        terms_ok = bool(np.isfinite(value))
+
+        for _ in range(max(3, args.warmup)):
+            step()
+        rt.synchronize()
+        d.barrier()
+        rt.synchronize()
+        launches0 = kernel.launches
+        with ClockSampler(d.local) as clocks:
+            total_ms, per_step = _time_steps(rt, step, args.steps)
+        launches = kernel.launches - launches0 + (args.steps if d.world > 1 else 0)
+        rt.synchronize()
+        d.barrier()
+        step_ms = d.max(total_ms / args.steps)
+        kern_ms = float(np.mean(per_step))
+        value_gbs = 8 * total_n / (step_ms * 1e-3) / 1e9
+
+        # e2e through the public API: pinned host -> device, reduce, scalar back
+        e2e_steps = max(2, min(args.steps, 5))
+        h2d = 2 * n * 4
+        gx2, gy2 = pool.alloc_uninitialized(nd.float32, (n,)), pool.alloc_uninitialized(nd.float32, (n,))
+
+        def e2e_step():
+            gx2.copy_from_host(hx, sync=False)
+            gy2.copy_from_host(hy, sync=False)
+            return kernel(gx2, gy2)          # returns the host scalar (4-byte DtoH)
+        e2e_step()
+        d.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        e2e_s = d.max((time.perf_counter() - t0) / e2e_steps)
+        e2e_gbs = 8 * total_n / e2e_s / 1e9
+        gx2.free()
+        gy2.free()
+
+        workloads = {} if args.quick or d.world > 1 else secondary_workloads(rt, nd, ew, rd, pool, peak)
+
+    algo_bytes = 8 * n
+    achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": d.world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(step_ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_per_gpu": n, "n_total": total_n,
+                   "variant": best, "autotune_seconds": round(tune_s, 2),
+                   "autotune_from_store": tuned.from_store,
+                   "l2": "inputs 2 GiB per GPU > 126 MB L2 (no flush needed)",
+                   "parallelism": f"shards{d.world}", "accumulator": "float64",
+                   "gpu": info["name"], "result_finite": terms_ok},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
+                     if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": _ncu_traffic("dot_k"),
+                     "kernel": kernel.launch_config(gx, gy)["entry"],
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "avg_kernel_ms": round(kern_ms, 4)},
+        "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 4, "steps": e2e_steps,
+                "path": "GPUArray.copy_from_host (pinned) x2 + ReductionKernel.__call__ "
+                        "(numpy scalar)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "workloads": workloads,
+    }
+    if d.world == 1 and d.rank == 0 and not args.no_cpu:
+        try:
+            base = cpu_reference("dot_k", budget_s=10.0)
+            line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind",
+                                                         "sample")}
+        except Exception as exc:  # pragma: no cover - report, don't fail the bench
+            line["cpu_baseline"] = {"value": None, "error": str(exc)}
+    if d.rank == 0:
+        print(json.dumps(line))
+    d.close()
+    return 0
+
+
+def _ncu_traffic(kernel: str):
+    """dram bytes per launch from the committed ncu summary, if captured."""
+    path = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        data = json.loads(path.read_text())
+        return data["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def secondary_workloads(rt, nd, ew, rd, pool, peak):
+    """The other BASELINE configs, single GPU, device-timed (best of 10)."""
+    out = {}
+    n = N_PER_GPU
+    rng = np.random.default_rng(1)
+
+    def best_ms(fn, reps=10):
+        fn()
+        rt.synchronize()
+        best = math.inf
+        for _ in range(reps):
+            ms, _ = _time_steps(rt, fn, 1)
+            best = min(best, ms)
+        return best
+
+    def record(name, fn, nbytes, **extra):
+        ms = best_ms(fn)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
+                     "algorithmic_bytes": nbytes, **extra}
+
+    x = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
+    y = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
+    z = pool.alloc_uninitialized(nd.float32, (n,))
+    axpy = ew.ElementwiseKernel("float a, float *x, float b, float *y, float *z",
+                                "z[i] = a * x[i] + b * y[i]", "axpy")
+    record("axpy_f32_2p28", lambda: axpy(2.0, x, -3.0, y, z), 12 * n,
+           variant=str(axpy.variant))
+    o32 = pool.alloc_uninitialized(nd.float32, ())
+    mx = rd.make_reduction("float *x", nd.float32, "0", "a > b ? a : b", "fabsf(x[i])",
+                           name="maxabs")
+    record("maxabs_f32_2p28", lambda: mx.launch(x, out=o32), 4 * n)
+    sq = rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i] * x[i]", name="sumsq")
+    record("l2sq_f32_2p28", lambda: sq.launch(x, out=o32), 4 * n)
+    for a in (x, y, z):
+        a.free()
+    xd = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
+    zd = pool.alloc_uninitialized(nd.float64, (n,))
+    ps = ew.ElementwiseKernel("double a, double *x, double *z",
+                              "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])", "polysin")
+    record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n)
+    xd.free()
+    zd.free()
+    xi = nd.from_host(pool, nd.int64, rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64))
+    o64 = pool.alloc_uninitialized(nd.int64, ())
+    si = rd.sum_kernel(nd.int64)
+    record("sum_i64_2p28", lambda: si.launch(xi, out=o64), 8 * n)
+    xi.free()
+    return out
+
+
+def main(argv=None) -> int:
+    p = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--quick", action="store_true", help="skip the secondary workloads")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    args = p.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

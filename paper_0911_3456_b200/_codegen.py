@@ -1,0 +1,236 @@
+"""Shared CUDA code generation and launch plumbing for the kernel templates.
+
+Both generators (elementwise, reduction) turn a parsed signature plus user C
+text into the placeholder bindings of a template under ``templates/``.  The
+interesting decision made here is whether the *vector path* may be emitted:
+
+* every occurrence of every vector parameter in the user text must be the
+  exact element reference ``name[i]`` (whitespace allowed), not address-taken
+  and not a member of something else;
+* then each vector is classified as read, written, or both -- the register
+  chunk is loaded only when read, stored only when written, and a vector that
+  is written conditionally (or only sometimes) is loaded first so untouched
+  elements are stored back unchanged.
+
+The same analysis generalises the reference's ``\\bi\\b`` rewriting trick
+(``src/elementwise.py:185,195-201``): instead of rewriting text, the user's
+statement becomes the body of a template function instantiated once with
+pointers and once with register ``rtcg::lane`` wrappers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import re
+from dataclasses import dataclass
+from functools import lru_cache
+from pathlib import Path
+
+from . import csyntax as cs
+
+TEMPLATES = Path(__file__).resolve().parent / "templates"
+
+_WIDE = {"i": ("long", ctypes.c_int64), "u": ("unsigned long", ctypes.c_uint64),
+         "f": ("double", ctypes.c_double)}
+
+CACHE_POLICIES = {
+    # name: (load policy for read-only vectors, load policy for read-write
+    #        vectors, store policy) -- see rtcg::ld16 / rtcg::st16
+    "default": (1, 0, 0),
+    "streaming": (2, 2, 1),
+    "no-l1": (3, 0, 2),
+}
+
+_CONTROL = re.compile(r"\b(?:if|else|for|while|do|switch|case|goto|return|break|continue)\b|[{}]")
+
+
+@lru_cache(maxsize=None)
+def template(name: str) -> str:
+    return (TEMPLATES / name).read_text()
+
+
+@dataclass(frozen=True)
+class Access:
+    read: bool
+    written: bool
+
+    @property
+    def used(self) -> bool:
+        return self.read or self.written
+
+
+def _occurrences(name: str, text: str):
+    """All uses of identifier *name* that are not member accesses."""
+    pat = re.compile(r"(?<![\w.])(?<!->)" + re.escape(name) + r"\b")
+    return list(pat.finditer(text))
+
+
+_REF_TAIL = re.compile(r"\s*\[\s*i\s*\]")
+_PURE_ASSIGN = re.compile(r"\s*=(?!=)")
+_COMPOUND = re.compile(r"\s*(?:<<|>>|[-+*/%&|^])=")
+_POSTFIX = re.compile(r"\s*(?:\+\+|--)")
+
+
+def analyze(text: str, vectors) -> dict | None:
+    """Per-vector :class:`Access` if the vector path is legal for *text*,
+    else None.  *vectors* are parameter names."""
+    result = {}
+    unconditional_stores = not _CONTROL.search(text)
+    for name in vectors:
+        read = written = False
+        for m in _occurrences(name, text):
+            tail = _REF_TAIL.match(text, m.end())
+            if tail is None:
+                return None  # x used as a pointer / with another index
+            before = text[:m.start()].rstrip()
+            if before.endswith("&") and not before.endswith("&&"):
+                return None  # address of the element
+            after = tail.end()
+            prefix_incdec = before.endswith("++") or before.endswith("--")
+            if prefix_incdec or _COMPOUND.match(text, after) or _POSTFIX.match(text, after):
+                read = written = True
+            elif _PURE_ASSIGN.match(text, after):
+                written = True
+                at_statement_start = before == "" or before.endswith(";")
+                if not (at_statement_start and unconditional_stores):
+                    read = True  # partial/conditional write: keep old values
+            else:
+                read = True
+        result[name] = Access(read, written)
+    return result
+
+
+def chunk_width(sig, access) -> int:
+    """Elements per 16-byte chunk: set by the narrowest accessed vector."""
+    sizes = [p.dtype.size for p in sig.vectors if access[p.name].used]
+    return 16 // min(sizes) if sizes else 0
+
+
+def parts(sig, access, width: int, policy: str) -> dict:
+    """Placeholder bindings shared by the elementwise and reduction templates."""
+    ld_ro, ld_rw, st = CACHE_POLICIES[policy]
+    vec_ok = access is not None and width > 0
+    op_tparams, op_params, kgen, kvec, unpack = [], [], [], [], []
+    ptr_gen, ptr_vec, lane_types, lane_args, call_args = [], [], [], [], []
+    decls, loads, stores = [], [], []
+    for p in sig.params:
+        c = p.dtype.cname
+        call_args.append(f", {p.name}")
+        if not p.is_vector:
+            wide = _WIDE[p.dtype.kind][0]
+            op_params.append(f", {c} {p.name}")
+            kgen.append(f"{wide} rtcg_w_{p.name}")
+            kvec.append(f"{wide} rtcg_w_{p.name}")
+            unpack.append(f"    {c} {p.name} = ({c}) rtcg_w_{p.name};")
+            lane_args.append(f", {p.name}")
+            continue
+        op_tparams.append(f"class rtcg_T_{p.name}")
+        op_params.append(f", rtcg_T_{p.name} {p.name}")
+        kgen.append(f"{c} *{p.name}")
+        ptr_gen.append(f"{c} *")
+        acc = access[p.name] if vec_ok else Access(True, True)
+        read_only = acc.read and not acc.written
+        qual = "const " if read_only else ""
+        kvec.append(f"{qual}{c} *__restrict__ {p.name}")
+        ptr_vec.append(f"{qual}{c} *")
+        if vec_ok and acc.used:
+            lane_types.append(f"rtcg::lane<{c}>")
+            lane_args.append(f", rtcg::lane<{c}>{{rtcg_v_{p.name}[u].e[k]}}")
+            decls.append(f"        rtcg::chunk<{c}, E> rtcg_v_{p.name}[U];")
+            if acc.read:
+                hint = ld_ro if read_only else ld_rw
+                loads.append(f"                rtcg::load<{hint}>(rtcg_v_{p.name}[u], {p.name}, cu);")
+            if acc.written:
+                stores.append(f"                rtcg::store<{st}>({p.name}, cu, rtcg_v_{p.name}[u]);")
+        else:
+            lane_types.append(f"{qual}{c} *")
+            lane_args.append(f", {p.name}")
+    return {
+        "vector": vec_ok,
+        "width": width,
+        "op_tparams": ", ".join(op_tparams),
+        "op_params": "".join(op_params),
+        "kparams_generic": ", ".join(kgen),
+        "kparams_vector": ", ".join(kvec),
+        "unpack": "\n".join(unpack),
+        "ptr_types_generic": ", ".join(ptr_gen),
+        "ptr_types_vector": ", ".join(ptr_vec),
+        "call_args": "".join(call_args),
+        "lane_types": ", ".join(lane_types),
+        "lane_args": "".join(lane_args),
+        "vec_decls": "\n".join(decls),
+        "vec_loads": "\n".join(loads),
+        "vec_stores": "\n".join(stores),
+    }
+
+
+def render(template_name: str, bindings: dict) -> str:
+    return cs.render(template(template_name),
+                     {"prelude": template("prelude.cuh").rstrip("\n"), **bindings})
+
+
+# --- launch plumbing ---------------------------------------------------------------------
+
+
+def scalar_value(value, dtype):
+    """Widen a Python/numpy scalar the way the reference does
+    (``src/elementwise.py:316-321``): float kinds -> double, unsigned ->
+    uint64 modulo 2**64, signed -> int64; the kernel casts to the declared
+    type."""
+    if dtype.kind == "f":
+        return ctypes.c_double(float(value))
+    if dtype.kind == "u":
+        return ctypes.c_uint64(int(value) & 0xFFFFFFFFFFFFFFFF)
+    return ctypes.c_int64(int(value))
+
+
+def pack(values) -> ctypes.Array:
+    """cuLaunchKernel parameter array: pointers to each ctypes value."""
+    arr = (ctypes.c_void_p * len(values))()
+    for k, v in enumerate(values):
+        arr[k] = ctypes.addressof(v)
+    return arr
+
+
+def vector_path_ok(entries, n: int) -> bool:
+    """entries: (index-0 address, local address, itemsize, Access) per used
+    vector.  True when every index-0 address is 16-byte aligned and no written
+    vector overlaps another used vector over the n local elements."""
+    spans = []
+    for addr0, local, size, acc in entries:
+        if addr0 % 16:
+            return False
+        spans.append((local, local + n * size, acc.written))
+    for a in range(len(spans)):
+        lo_a, hi_a, w_a = spans[a]
+        for b in range(a + 1, len(spans)):
+            lo_b, hi_b, w_b = spans[b]
+            if (w_a or w_b) and lo_a < hi_b and lo_b < hi_a:
+                return False
+    return True
+
+
+_sm_count: dict[int, int] = {}
+
+
+def sm_count(device: int) -> int:
+    hit = _sm_count.get(device)
+    if hit is None:
+        from . import _runtime
+        hit = _sm_count[device] = _runtime.device_info(device)["sm_count"]
+    return hit
+
+
+def grid_for(function: int, device: int, block: int, workers: int | None,
+             n: int, per_thread: int) -> int:
+    """CTAs to launch: explicit ``workers``, else enough resident CTAs to
+    fill every SM once (persistent-style), never more than the work needs."""
+    from . import _runtime
+    useful = max(1, math.ceil(n / (block * per_thread)))
+    if workers is not None:
+        grid = workers
+    else:
+        resident = sm_count(device) * max(1, _runtime.occupancy(function, block))
+        grid = min(resident, useful)
+    return max(1, min(grid, 2**31 - 1))

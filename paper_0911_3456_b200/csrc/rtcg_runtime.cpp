@@ -1,0 +1,581 @@
+// librtcg_b200.so -- NVRTC + CUDA driver runtime behind the C ABI declared in
+// include/rtcg_b200.h.  See that header for which reference seam each entry
+// point replaces.
+//
+// Design notes
+//  * libcuda.so.1 and libnvrtc.so.12 are dlopen'd on first use, so the library
+//    loads on GPU-less build hosts (where NVRTC still compiles sm_100a cubins).
+//  * Contexts: the device's *primary* context is retained and made current, so
+//    modules, allocations and streams interoperate with the CUDA runtime (and
+//    torch) in the same process.
+//  * Errors: every call returns an rtcg_status and stores a message in a
+//    thread-local buffer read by rtcg_last_error().
+
+#include "../../include/rtcg_b200.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int status, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_error = buf;
+    return status;
+}
+
+// ---------------------------------------------------------------- driver API
+
+template <class Sig>
+using fnptr = Sig *;
+
+struct Driver {
+    bool tried = false;
+    void *handle = nullptr;
+    std::string why;
+#define RTCG_DRIVER_FNS(X)                                                     \
+    X(cuInit, CUresult(unsigned))                                          \
+    X(cuDriverGetVersion, CUresult(int *))                                 \
+    X(cuDeviceGetCount, CUresult(int *))                                   \
+    X(cuDeviceGet, CUresult(CUdevice *, int))                              \
+    X(cuDeviceGetName, CUresult(char *, int, CUdevice))                    \
+    X(cuDeviceGetAttribute, CUresult(int *, CUdevice_attribute, CUdevice)) \
+    X(cuDeviceTotalMem_v2, CUresult(size_t *, CUdevice))                   \
+    X(cuDevicePrimaryCtxRetain, CUresult(CUcontext *, CUdevice))           \
+    X(cuCtxSetCurrent, CUresult(CUcontext))                                \
+    X(cuCtxGetCurrent, CUresult(CUcontext *))                              \
+    X(cuCtxGetDevice, CUresult(CUdevice *))                                \
+    X(cuCtxSynchronize, CUresult(void))                                    \
+    X(cuMemGetInfo_v2, CUresult(size_t *, size_t *))                       \
+    X(cuModuleLoadData, CUresult(CUmodule *, const void *))                \
+    X(cuModuleUnload, CUresult(CUmodule))                                  \
+    X(cuModuleGetFunction, CUresult(CUfunction *, CUmodule, const char *)) \
+    X(cuFuncGetAttribute, CUresult(int *, CUfunction_attribute, CUfunction)) \
+    X(cuOccupancyMaxActiveBlocksPerMultiprocessor,                             \
+      CUresult(int *, CUfunction, int, size_t))                            \
+    X(cuLaunchKernel, CUresult(CUfunction, unsigned, unsigned, unsigned,   \
+                                   unsigned, unsigned, unsigned, unsigned,     \
+                                   CUstream, void **, void **))                \
+    X(cuMemAlloc_v2, CUresult(CUdeviceptr *, size_t))                      \
+    X(cuMemFree_v2, CUresult(CUdeviceptr))                                 \
+    X(cuMemsetD8Async, CUresult(CUdeviceptr, unsigned char, size_t, CUstream)) \
+    X(cuMemcpyHtoDAsync_v2,                                                    \
+      CUresult(CUdeviceptr, const void *, size_t, CUstream))               \
+    X(cuMemcpyDtoHAsync_v2, CUresult(void *, CUdeviceptr, size_t, CUstream)) \
+    X(cuMemcpyDtoDAsync_v2,                                                    \
+      CUresult(CUdeviceptr, CUdeviceptr, size_t, CUstream))                \
+    X(cuMemHostAlloc, CUresult(void **, size_t, unsigned))                 \
+    X(cuMemFreeHost, CUresult(void *))                                     \
+    X(cuMemHostRegister_v2, CUresult(void *, size_t, unsigned))            \
+    X(cuMemHostUnregister, CUresult(void *))                               \
+    X(cuStreamCreate, CUresult(CUstream *, unsigned))                      \
+    X(cuStreamDestroy_v2, CUresult(CUstream))                              \
+    X(cuStreamSynchronize, CUresult(CUstream))                             \
+    X(cuEventCreate, CUresult(CUevent *, unsigned))                        \
+    X(cuEventDestroy_v2, CUresult(CUevent))                                \
+    X(cuEventRecord, CUresult(CUevent, CUstream))                          \
+    X(cuEventSynchronize, CUresult(CUevent))                               \
+    X(cuEventElapsedTime, CUresult(float *, CUevent, CUevent))             \
+    X(cuGetErrorName, CUresult(CUresult, const char **))                   \
+    X(cuGetErrorString, CUresult(CUresult, const char **))
+#define RTCG_DECLARE(name, sig) fnptr<sig> name = nullptr;
+    RTCG_DRIVER_FNS(RTCG_DECLARE)
+#undef RTCG_DECLARE
+    int init_status = RTCG_ERR_NO_DEVICE;
+};
+
+Driver g_drv;
+std::mutex g_drv_mutex;
+std::vector<CUcontext> g_primary;  // per device, retained once
+thread_local int t_device = -1;
+
+const char *cu_name(CUresult r) {
+    const char *s = nullptr;
+    if (g_drv.cuGetErrorName && g_drv.cuGetErrorName(r, &s) == CUDA_SUCCESS && s)
+        return s;
+    return "CUDA_ERROR_?";
+}
+
+const char *cu_text(CUresult r) {
+    const char *s = nullptr;
+    if (g_drv.cuGetErrorString && g_drv.cuGetErrorString(r, &s) == CUDA_SUCCESS && s)
+        return s;
+    return "";
+}
+
+int cu_fail(CUresult r, const char *what) {
+    int status = RTCG_ERR_CUDA;
+    if (r == CUDA_ERROR_OUT_OF_MEMORY) status = RTCG_ERR_OUT_OF_MEMORY;
+    else if (r == CUDA_ERROR_NOT_FOUND) status = RTCG_ERR_NOT_FOUND;
+    else if (r == CUDA_ERROR_INVALID_IMAGE || r == CUDA_ERROR_NO_BINARY_FOR_GPU ||
+             r == CUDA_ERROR_INVALID_PTX || r == CUDA_ERROR_UNSUPPORTED_PTX_VERSION)
+        status = RTCG_ERR_LOAD;
+    else if (r == CUDA_ERROR_NO_DEVICE) status = RTCG_ERR_NO_DEVICE;
+    return fail(status, "%s failed: %s (%d) %s", what, cu_name(r), (int)r, cu_text(r));
+}
+
+// Load libcuda and cuInit once; later calls return the cached outcome.
+int driver_ready() {
+    std::lock_guard<std::mutex> lock(g_drv_mutex);
+    if (g_drv.tried) {
+        if (g_drv.init_status != RTCG_OK) return fail(g_drv.init_status, "%s", g_drv.why.c_str());
+        return RTCG_OK;
+    }
+    g_drv.tried = true;
+    g_drv.handle = dlopen("libcuda.so.1", RTLD_NOW | RTLD_LOCAL);
+    if (!g_drv.handle) {
+        g_drv.why = std::string("cannot load libcuda.so.1 (no NVIDIA driver): ") + dlerror();
+        return fail(g_drv.init_status, "%s", g_drv.why.c_str());
+    }
+#define RTCG_RESOLVE(name, sig)                                                    \
+    g_drv.name = reinterpret_cast<fnptr<sig>>(dlsym(g_drv.handle, #name));          \
+    if (!g_drv.name) {                                                             \
+        g_drv.why = "libcuda.so.1 lacks symbol " #name;                            \
+        return fail(g_drv.init_status, "%s", g_drv.why.c_str());                   \
+    }
+    RTCG_DRIVER_FNS(RTCG_RESOLVE)
+#undef RTCG_RESOLVE
+    CUresult r = g_drv.cuInit(0);
+    if (r != CUDA_SUCCESS) {
+        g_drv.why = std::string("cuInit failed: ") + cu_name(r) + " " + cu_text(r);
+        return fail(g_drv.init_status, "%s", g_drv.why.c_str());
+    }
+    int count = 0;
+    if (g_drv.cuDeviceGetCount(&count) != CUDA_SUCCESS || count == 0) {
+        g_drv.why = "no CUDA device visible";
+        return fail(g_drv.init_status, "%s", g_drv.why.c_str());
+    }
+    g_primary.assign(count, nullptr);
+    g_drv.init_status = RTCG_OK;
+    return RTCG_OK;
+}
+
+// Make sure the calling thread has a current context (device 0 by default,
+// or the device torch / the caller already made current).
+int ensure_context() {
+    int s = driver_ready();
+    if (s != RTCG_OK) return s;
+    if (t_device >= 0) return RTCG_OK;
+    CUcontext cur = nullptr;
+    if (g_drv.cuCtxGetCurrent(&cur) == CUDA_SUCCESS && cur) {
+        CUdevice dev;
+        if (g_drv.cuCtxGetDevice(&dev) == CUDA_SUCCESS) {
+            t_device = (int)dev;
+            return RTCG_OK;
+        }
+    }
+    return rtcg_set_device(0);
+}
+
+#define CU_CALL(expr, what)                          \
+    do {                                             \
+        CUresult r_ = (expr);                        \
+        if (r_ != CUDA_SUCCESS) return cu_fail(r_, what); \
+    } while (0)
+
+#define NEED_CONTEXT()                      \
+    do {                                    \
+        int s_ = ensure_context();          \
+        if (s_ != RTCG_OK) return s_;       \
+    } while (0)
+
+// ---------------------------------------------------------------- NVRTC
+
+typedef int nvrtcResult_t;
+struct Nvrtc {
+    bool tried = false;
+    void *handle = nullptr;
+    std::string why;
+    nvrtcResult_t (*nvrtcVersion)(int *, int *) = nullptr;
+    nvrtcResult_t (*nvrtcCreateProgram)(void **, const char *, const char *, int,
+                                        const char *const *, const char *const *) = nullptr;
+    nvrtcResult_t (*nvrtcDestroyProgram)(void **) = nullptr;
+    nvrtcResult_t (*nvrtcCompileProgram)(void *, int, const char *const *) = nullptr;
+    nvrtcResult_t (*nvrtcGetCUBINSize)(void *, size_t *) = nullptr;
+    nvrtcResult_t (*nvrtcGetCUBIN)(void *, char *) = nullptr;
+    nvrtcResult_t (*nvrtcGetProgramLogSize)(void *, size_t *) = nullptr;
+    nvrtcResult_t (*nvrtcGetProgramLog)(void *, char *) = nullptr;
+    const char *(*nvrtcGetErrorString)(nvrtcResult_t) = nullptr;
+};
+
+Nvrtc g_nvrtc;
+std::mutex g_nvrtc_mutex;
+
+int nvrtc_ready() {
+    std::lock_guard<std::mutex> lock(g_nvrtc_mutex);
+    if (g_nvrtc.tried) {
+        if (!g_nvrtc.handle) return fail(RTCG_ERR_NO_COMPILER, "%s", g_nvrtc.why.c_str());
+        return RTCG_OK;
+    }
+    g_nvrtc.tried = true;
+    const char *env = getenv("RTCG_NVRTC_LIBRARY");
+    const char *candidates[] = {env, "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                                "libnvrtc.so"};
+    for (const char *c : candidates) {
+        if (!c || !*c) continue;
+        g_nvrtc.handle = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+        if (g_nvrtc.handle) break;
+    }
+    if (!g_nvrtc.handle) {
+        g_nvrtc.why = std::string("cannot load libnvrtc.so.12: ") + dlerror();
+        return fail(RTCG_ERR_NO_COMPILER, "%s", g_nvrtc.why.c_str());
+    }
+#define RTCG_NV(name)                                                             \
+    *reinterpret_cast<void **>(&g_nvrtc.name) = dlsym(g_nvrtc.handle, #name);     \
+    if (!g_nvrtc.name) {                                                          \
+        g_nvrtc.why = "libnvrtc lacks symbol " #name;                             \
+        dlclose(g_nvrtc.handle);                                                  \
+        g_nvrtc.handle = nullptr;                                                 \
+        return fail(RTCG_ERR_NO_COMPILER, "%s", g_nvrtc.why.c_str());             \
+    }
+    RTCG_NV(nvrtcVersion)
+    RTCG_NV(nvrtcCreateProgram)
+    RTCG_NV(nvrtcDestroyProgram)
+    RTCG_NV(nvrtcCompileProgram)
+    RTCG_NV(nvrtcGetCUBINSize)
+    RTCG_NV(nvrtcGetCUBIN)
+    RTCG_NV(nvrtcGetProgramLogSize)
+    RTCG_NV(nvrtcGetProgramLog)
+    RTCG_NV(nvrtcGetErrorString)
+#undef RTCG_NV
+    return RTCG_OK;
+}
+
+char *dup_string(const std::string &s) {
+    char *p = static_cast<char *>(malloc(s.size() + 1));
+    if (p) memcpy(p, s.c_str(), s.size() + 1);
+    return p;
+}
+
+}  // namespace
+
+// ============================================================== public ABI
+
+extern "C" {
+
+int rtcg_abi_version(void) { return RTCG_ABI_VERSION; }
+
+const char *rtcg_last_error(void) { return g_error.c_str(); }
+
+void rtcg_free_buffer(void *p) { free(p); }
+
+int rtcg_nvrtc_version(int *major, int *minor) {
+    int s = nvrtc_ready();
+    if (s != RTCG_OK) return s;
+    if (g_nvrtc.nvrtcVersion(major, minor) != 0) return fail(RTCG_ERR_NO_COMPILER, "nvrtcVersion failed");
+    return RTCG_OK;
+}
+
+int rtcg_compile(const char *source, const char *program_name, const char *const *options,
+                 int num_options, void **image, size_t *image_size, char **log) {
+    if (image) *image = nullptr;
+    if (image_size) *image_size = 0;
+    if (log) *log = nullptr;
+    if (!source || !image || !image_size || num_options < 0)
+        return fail(RTCG_ERR_INVALID, "rtcg_compile: null argument");
+    int s = nvrtc_ready();
+    if (s != RTCG_OK) return s;
+    void *prog = nullptr;
+    int r = g_nvrtc.nvrtcCreateProgram(&prog, source, program_name ? program_name : "rtcg.cu",
+                                       0, nullptr, nullptr);
+    if (r != 0)
+        return fail(RTCG_ERR_COMPILE, "nvrtcCreateProgram: %s", g_nvrtc.nvrtcGetErrorString(r));
+    int cr = g_nvrtc.nvrtcCompileProgram(prog, num_options, options);
+    size_t log_size = 0;
+    std::string text;
+    if (g_nvrtc.nvrtcGetProgramLogSize(prog, &log_size) == 0 && log_size > 1) {
+        text.resize(log_size);
+        g_nvrtc.nvrtcGetProgramLog(prog, &text[0]);
+        text.resize(strlen(text.c_str()));
+    }
+    if (log) *log = dup_string(text);
+    if (cr != 0) {
+        g_nvrtc.nvrtcDestroyProgram(&prog);
+        return fail(RTCG_ERR_COMPILE, "nvrtcCompileProgram: %s", g_nvrtc.nvrtcGetErrorString(cr));
+    }
+    size_t n = 0;
+    if (g_nvrtc.nvrtcGetCUBINSize(prog, &n) != 0 || n == 0) {
+        g_nvrtc.nvrtcDestroyProgram(&prog);
+        return fail(RTCG_ERR_COMPILE,
+                    "NVRTC produced no cubin (is -arch=sm_XXX a real architecture?)");
+    }
+    char *buf = static_cast<char *>(malloc(n));
+    if (!buf) {
+        g_nvrtc.nvrtcDestroyProgram(&prog);
+        return fail(RTCG_ERR_OUT_OF_MEMORY, "host malloc(%zu) failed", n);
+    }
+    g_nvrtc.nvrtcGetCUBIN(prog, buf);
+    g_nvrtc.nvrtcDestroyProgram(&prog);
+    *image = buf;
+    *image_size = n;
+    return RTCG_OK;
+}
+
+int rtcg_init(void) { return driver_ready(); }
+
+int rtcg_device_count(int *count) {
+    int s = driver_ready();
+    if (s != RTCG_OK) return s;
+    CU_CALL(g_drv.cuDeviceGetCount(count), "cuDeviceGetCount");
+    return RTCG_OK;
+}
+
+int rtcg_device_info_get(int device, rtcg_device_info *info) {
+    int s = driver_ready();
+    if (s != RTCG_OK) return s;
+    if (!info) return fail(RTCG_ERR_INVALID, "null info");
+    memset(info, 0, sizeof *info);
+    CUdevice dev;
+    CU_CALL(g_drv.cuDeviceGet(&dev, device), "cuDeviceGet");
+    CU_CALL(g_drv.cuDeviceGetName(info->name, sizeof info->name - 1, dev), "cuDeviceGetName");
+    struct { int *dst; CUdevice_attribute a; } attrs[] = {
+        {&info->cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR},
+        {&info->cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR},
+        {&info->sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT},
+        {&info->max_threads_per_sm, CU_DEVICE_ATTRIBUTE_MAX_THREADS_PER_MULTIPROCESSOR},
+        {&info->max_threads_per_block, CU_DEVICE_ATTRIBUTE_MAX_THREADS_PER_BLOCK},
+        {&info->l2_bytes, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE},
+        {&info->mem_clock_khz, CU_DEVICE_ATTRIBUTE_MEMORY_CLOCK_RATE},
+        {&info->mem_bus_width, CU_DEVICE_ATTRIBUTE_GLOBAL_MEMORY_BUS_WIDTH},
+    };
+    for (auto &a : attrs) CU_CALL(g_drv.cuDeviceGetAttribute(a.dst, a.a, dev), "cuDeviceGetAttribute");
+    size_t total = 0;
+    CU_CALL(g_drv.cuDeviceTotalMem_v2(&total, dev), "cuDeviceTotalMem");
+    info->total_mem = total;
+    CU_CALL(g_drv.cuDriverGetVersion(&info->driver_version), "cuDriverGetVersion");
+    return RTCG_OK;
+}
+
+int rtcg_set_device(int device) {
+    int s = driver_ready();
+    if (s != RTCG_OK) return s;
+    if (device < 0 || device >= (int)g_primary.size())
+        return fail(RTCG_ERR_INVALID, "device %d out of range [0, %zu)", device, g_primary.size());
+    CUcontext ctx;
+    {
+        std::lock_guard<std::mutex> lock(g_drv_mutex);
+        if (!g_primary[device]) {
+            CUdevice dev;
+            CU_CALL(g_drv.cuDeviceGet(&dev, device), "cuDeviceGet");
+            CU_CALL(g_drv.cuDevicePrimaryCtxRetain(&g_primary[device], dev),
+                    "cuDevicePrimaryCtxRetain");
+        }
+        ctx = g_primary[device];
+    }
+    CU_CALL(g_drv.cuCtxSetCurrent(ctx), "cuCtxSetCurrent");
+    t_device = device;
+    return RTCG_OK;
+}
+
+int rtcg_get_device(int *device) {
+    NEED_CONTEXT();
+    *device = t_device;
+    return RTCG_OK;
+}
+
+int rtcg_synchronize(void) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuCtxSynchronize(), "cuCtxSynchronize");
+    return RTCG_OK;
+}
+
+int rtcg_mem_get_info(uint64_t *free_bytes, uint64_t *total_bytes) {
+    NEED_CONTEXT();
+    size_t f = 0, t = 0;
+    CU_CALL(g_drv.cuMemGetInfo_v2(&f, &t), "cuMemGetInfo");
+    *free_bytes = f;
+    *total_bytes = t;
+    return RTCG_OK;
+}
+
+int rtcg_module_load(const void *image, size_t image_size, rtcg_module_t *module) {
+    if (!image || !module || image_size < 4)
+        return fail(RTCG_ERR_INVALID, "rtcg_module_load: empty image");
+    NEED_CONTEXT();
+    CUmodule m;
+    CU_CALL(g_drv.cuModuleLoadData(&m, image), "cuModuleLoadData");
+    *module = reinterpret_cast<rtcg_module_t>(m);
+    return RTCG_OK;
+}
+
+int rtcg_module_unload(rtcg_module_t module) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuModuleUnload(reinterpret_cast<CUmodule>(module)), "cuModuleUnload");
+    return RTCG_OK;
+}
+
+int rtcg_module_function(rtcg_module_t module, const char *name, rtcg_function_t *function) {
+    NEED_CONTEXT();
+    CUfunction f;
+    CUresult r = g_drv.cuModuleGetFunction(&f, reinterpret_cast<CUmodule>(module), name);
+    if (r == CUDA_ERROR_NOT_FOUND) return fail(RTCG_ERR_NOT_FOUND, "kernel symbol '%s' not found", name);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction");
+    *function = reinterpret_cast<rtcg_function_t>(f);
+    return RTCG_OK;
+}
+
+int rtcg_function_occupancy(rtcg_function_t function, int block_threads, size_t dynamic_smem,
+                            int *blocks_per_sm) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuOccupancyMaxActiveBlocksPerMultiprocessor(
+                blocks_per_sm, reinterpret_cast<CUfunction>(function), block_threads, dynamic_smem),
+            "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+    return RTCG_OK;
+}
+
+int rtcg_function_registers(rtcg_function_t function, int *num_regs) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuFuncGetAttribute(num_regs, CU_FUNC_ATTRIBUTE_NUM_REGS,
+                                     reinterpret_cast<CUfunction>(function)),
+            "cuFuncGetAttribute");
+    return RTCG_OK;
+}
+
+int rtcg_launch(rtcg_function_t function, unsigned grid, unsigned block, unsigned dynamic_smem,
+                rtcg_stream_t stream, void **params) {
+    if (!function || grid == 0 || block == 0)
+        return fail(RTCG_ERR_INVALID, "rtcg_launch: grid=%u block=%u", grid, block);
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuLaunchKernel(reinterpret_cast<CUfunction>(function), grid, 1, 1, block, 1, 1,
+                                 dynamic_smem, reinterpret_cast<CUstream>(stream), params, nullptr),
+            "cuLaunchKernel");
+    return RTCG_OK;
+}
+
+int rtcg_mem_alloc(uint64_t nbytes, uint64_t *dptr) {
+    NEED_CONTEXT();
+    CUdeviceptr p = 0;
+    CU_CALL(g_drv.cuMemAlloc_v2(&p, nbytes), "cuMemAlloc");
+    *dptr = p;
+    return RTCG_OK;
+}
+
+int rtcg_mem_free(uint64_t dptr) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemFree_v2(dptr), "cuMemFree");
+    return RTCG_OK;
+}
+
+int rtcg_memset_async(uint64_t dptr, unsigned char value, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemsetD8Async(dptr, value, nbytes, reinterpret_cast<CUstream>(stream)),
+            "cuMemsetD8Async");
+    return RTCG_OK;
+}
+
+int rtcg_memcpy_htod_async(uint64_t dst, const void *src, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemcpyHtoDAsync_v2(dst, src, nbytes, reinterpret_cast<CUstream>(stream)),
+            "cuMemcpyHtoDAsync");
+    return RTCG_OK;
+}
+
+int rtcg_memcpy_dtoh_async(void *dst, uint64_t src, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemcpyDtoHAsync_v2(dst, src, nbytes, reinterpret_cast<CUstream>(stream)),
+            "cuMemcpyDtoHAsync");
+    return RTCG_OK;
+}
+
+int rtcg_memcpy_dtod_async(uint64_t dst, uint64_t src, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemcpyDtoDAsync_v2(dst, src, nbytes, reinterpret_cast<CUstream>(stream)),
+            "cuMemcpyDtoDAsync");
+    return RTCG_OK;
+}
+
+int rtcg_host_alloc(uint64_t nbytes, void **ptr) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemHostAlloc(ptr, nbytes, CU_MEMHOSTALLOC_PORTABLE), "cuMemHostAlloc");
+    return RTCG_OK;
+}
+
+int rtcg_host_free(void *ptr) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemFreeHost(ptr), "cuMemFreeHost");
+    return RTCG_OK;
+}
+
+int rtcg_host_register(void *ptr, uint64_t nbytes) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemHostRegister_v2(ptr, nbytes, CU_MEMHOSTREGISTER_PORTABLE),
+            "cuMemHostRegister");
+    return RTCG_OK;
+}
+
+int rtcg_host_unregister(void *ptr) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemHostUnregister(ptr), "cuMemHostUnregister");
+    return RTCG_OK;
+}
+
+int rtcg_stream_create(rtcg_stream_t *stream) {
+    NEED_CONTEXT();
+    CUstream s;
+    CU_CALL(g_drv.cuStreamCreate(&s, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+    *stream = reinterpret_cast<rtcg_stream_t>(s);
+    return RTCG_OK;
+}
+
+int rtcg_stream_destroy(rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuStreamDestroy_v2(reinterpret_cast<CUstream>(stream)), "cuStreamDestroy");
+    return RTCG_OK;
+}
+
+int rtcg_stream_synchronize(rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuStreamSynchronize(reinterpret_cast<CUstream>(stream)), "cuStreamSynchronize");
+    return RTCG_OK;
+}
+
+int rtcg_event_create(rtcg_event_t *event) {
+    NEED_CONTEXT();
+    CUevent e;
+    CU_CALL(g_drv.cuEventCreate(&e, CU_EVENT_DEFAULT), "cuEventCreate");
+    *event = reinterpret_cast<rtcg_event_t>(e);
+    return RTCG_OK;
+}
+
+int rtcg_event_destroy(rtcg_event_t event) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuEventDestroy_v2(reinterpret_cast<CUevent>(event)), "cuEventDestroy");
+    return RTCG_OK;
+}
+
+int rtcg_event_record(rtcg_event_t event, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuEventRecord(reinterpret_cast<CUevent>(event), reinterpret_cast<CUstream>(stream)),
+            "cuEventRecord");
+    return RTCG_OK;
+}
+
+int rtcg_event_synchronize(rtcg_event_t event) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuEventSynchronize(reinterpret_cast<CUevent>(event)), "cuEventSynchronize");
+    return RTCG_OK;
+}
+
+int rtcg_event_elapsed_ms(rtcg_event_t start, rtcg_event_t end, float *ms) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuEventElapsedTime(ms, reinterpret_cast<CUevent>(start),
+                                     reinterpret_cast<CUevent>(end)),
+            "cuEventElapsedTime");
+    return RTCG_OK;
+}
+
+}  // extern "C"

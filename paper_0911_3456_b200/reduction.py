@@ -1,0 +1,347 @@
+"""Generated reductions on the GPU: sums, extrema, inner products and kin.
+
+B200 version of the reference's ``src/reduction.py``.  A reduction is a
+signature plus three pieces of C: ``map_expr`` (one value per index ``i``,
+default: the first vector's element), ``reduce_expr`` over ``a`` and ``b``
+(assumed commutative and associative) and a ``neutral`` literal (the fold's
+identity, interpreted by the compiler, never by Python -- ``INT64_MIN`` and
+``-INFINITY`` work as written).
+
+Execution is two-stage like the reference (workers -> partials -> ordered
+combine), mapped onto one launch of ``templates/reduction.cu``:
+
+1. every CTA (a "worker") folds its index range with a thread-serial fold,
+   a warp-shuffle tree and a shared-memory tree into one partial;
+2. the last CTA to finish folds the partials in ascending CTA order.
+
+Accumulation uses the out dtype, except float32 accumulates in float64 and
+rounds once (``src/reduction.py:18-20,53-54``).  A fixed (n, variant) gives a
+bitwise-identical result on every run: no float atomics, fixed tree order.
+
+Both constructor forms are accepted: the reference's
+``ReductionKernel(spec, name, variant, ...)`` and PyCUDA's
+``ReductionKernel(dtype_out, neutral, reduce_expr, map_expr=None,
+arguments=None, name=...)``.  Calls return a numpy scalar of the out dtype
+(reference behaviour); ``return_device=True`` (the default in the PyCUDA form)
+returns a 0-d GPUArray instead, without a host synchronisation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _codegen as cg
+from . import jit
+from . import ndarray as nd
+from .elementwise import (KernelSignature, ParseError, VariantParams, _CHUNK_TOKEN,
+                          _check_name, _marshal, parse_signature)
+from .ndarray import Dtype
+
+__all__ = [
+    "NonScalarResult", "ReductionSpec", "ReductionKernel", "make_reduction",
+    "generate_reduction_source", "sum_kernel", "max_kernel", "min_kernel",
+    "dot_kernel",
+]
+
+
+class NonScalarResult(Exception):
+    """map/reduce expressions cannot produce one value per element/pair."""
+
+
+_AB = re.compile(r"\b([ab])\b")
+_DRIVER_NAMES = ("acc", "out", "partials", "result")
+
+
+def _accumulator_dtype(out_dtype: Dtype) -> Dtype:
+    return nd.float64 if out_dtype == nd.float32 else out_dtype
+
+
+@dataclass(frozen=True)
+class ReductionSpec:
+    """What to fold (``src/reduction.py:57-95``)."""
+
+    signature: KernelSignature
+    out_dtype: Dtype
+    neutral: str
+    reduce_expr: str
+    map_expr: str | None = None
+
+    def __post_init__(self) -> None:
+        if isinstance(self.signature, str):
+            object.__setattr__(self, "signature", parse_signature(self.signature))
+        object.__setattr__(self, "out_dtype", nd.dtype_of(self.out_dtype))
+        for p in self.signature.params:
+            if p.name in _DRIVER_NAMES:
+                raise ParseError(f"parameter name {p.name!r} collides with reduction "
+                                 f"driver identifiers")
+        if {m.group(1) for m in _AB.finditer(self.reduce_expr)} != {"a", "b"}:
+            raise NonScalarResult("reduce_expr must combine both operands a and b")
+        if not self.mapped.strip():
+            raise NonScalarResult("map_expr must produce a value per element")
+
+    @property
+    def mapped(self) -> str:
+        return self.map_expr if self.map_expr is not None else \
+            f"{self.signature.vectors[0].name}[i]"
+
+    @property
+    def acc_dtype(self) -> Dtype:
+        return _accumulator_dtype(self.out_dtype)
+
+
+def generate_reduction_source(spec: ReductionSpec, name: str,
+                              variant: VariantParams) -> str:
+    """CUDA source with ``<name>`` (vector path, when legal), ``<name>_g``
+    (general) and ``<name>_combine`` (ordered fold of partials)."""
+    _check_name(name)
+    sig = spec.signature
+    access = cg.analyze(spec.mapped, [p.name for p in sig.vectors])
+    if access is not None and any(a.written for a in access.values()):
+        access = None  # a map expression with side effects stays general
+    width = cg.chunk_width(sig, access) if access is not None else 0
+    b = cg.parts(sig, access, width, variant.cache)
+    b["map_tparams"] = b.pop("op_tparams")
+    b["map_params"] = b.pop("op_params")
+    b.update(name=name, unroll=variant.unroll, block=variant.block, chunking=_CHUNK_TOKEN[variant.chunking],
+             acc_t=spec.acc_dtype.cname, out_t=spec.out_dtype.cname,
+             neutral=spec.neutral, reduce_expr=spec.reduce_expr, map_expr=spec.mapped)
+    return cg.render("reduction.cu", b)
+
+
+class _Scratch:
+    """Per-device partials / result / out / ticket buffers of one kernel."""
+
+    def __init__(self, acc_size: int, out_size: int) -> None:
+        from . import _runtime
+        self.capacity = 0
+        self.partials = 0
+        self.acc_size, self.out_size = acc_size, out_size
+        self.result = _runtime.mem_alloc(64)
+        self.out = self.result + 16
+        self.ticket = self.result + 32
+        _runtime.memset_async(self.result, 0, 64)
+
+    def ensure(self, count: int) -> None:
+        from . import _runtime
+        if count > self.capacity:
+            if self.partials:
+                _runtime.synchronize()
+                _runtime.mem_free(self.partials)
+            cap = max(count, 2048)
+            self.partials = _runtime.mem_alloc(cap * self.acc_size)
+            self.capacity = cap
+
+
+def _is_dtype_like(obj) -> bool:
+    if isinstance(obj, Dtype):
+        return True
+    if isinstance(obj, (ReductionSpec, str)):
+        return False
+    try:
+        np.dtype(obj)
+        return True
+    except TypeError:
+        return False
+
+
+class ReductionKernel:
+    """A compiled reduction; ``kernel(args..., n=count)`` returns the result.
+
+    Construction: ``ReductionKernel(spec, name="reduce", variant=None, *,
+    config, cache, debug)`` (reference) or ``ReductionKernel(dtype_out,
+    neutral, reduce_expr, map_expr=None, arguments=None, name=..., ...)``
+    (PyCUDA; ``arguments`` is the signature text).
+    """
+
+    def __init__(self, *args, **kwargs) -> None:
+        if args and _is_dtype_like(args[0]) or "dtype_out" in kwargs:
+            self._init_pycuda(*args, **kwargs)
+        else:
+            self._init_reference(*args, **kwargs)
+
+    def _init_pycuda(self, dtype_out=None, neutral=None, reduce_expr=None, map_expr=None,
+                     arguments=None, name="reduce_kernel", variant=None, *,
+                     config=None, cache=None, debug=False, return_device=True, **_ignored):
+        if arguments is None:
+            raise ParseError("ReductionKernel needs an 'arguments' signature")
+        spec = ReductionSpec(arguments, nd.dtype_of(dtype_out), str(neutral), reduce_expr,
+                             map_expr)
+        self._init_reference(spec, name, variant, config=config, cache=cache, debug=debug)
+        self.return_device = return_device
+
+    def _init_reference(self, spec: ReductionSpec, name: str = "reduce",
+                        variant: VariantParams | None = None, *,
+                        config: jit.ToolchainConfig | None = None,
+                        cache: jit.CacheStore | None = None, debug: bool = False) -> None:
+        self.spec = spec
+        self.name = name
+        self.variant = (variant or VariantParams()).resolved()
+        self.return_device = False
+        self.source = generate_reduction_source(spec, name, self.variant)
+        sig = spec.signature
+        access = cg.analyze(spec.mapped, [p.name for p in sig.vectors])
+        if access is not None and any(a.written for a in access.values()):
+            access = None
+        self.access = access
+        self.width = cg.chunk_width(sig, access) if access is not None else 0
+        self.module = jit.compile(self.source, config, cache)
+        self.generic = jit.get_kernel(self.module, f"{name}_g")
+        self.vectorized = jit.get_kernel(self.module, name) if self.access and self.width else None
+        self.combine = jit.get_kernel(self.module, f"{name}_combine")
+        self._acc_ctype = nd.ctype_for(spec.acc_dtype)
+        self._scratch: dict[int, _Scratch] = {}
+        self._lock = threading.Lock()
+        self.launches = 0
+        if debug:
+            self._check_neutral()
+
+    def __repr__(self) -> str:
+        return (f"<ReductionKernel {self.name} [{self.spec.signature.render()}]"
+                f" -> {self.spec.out_dtype.name}>")
+
+    # -- plumbing --
+
+    def scratch(self, device: int) -> _Scratch:
+        with self._lock:
+            s = self._scratch.get(device)
+            if s is None:
+                s = self._scratch[device] = _Scratch(self.spec.acc_dtype.size,
+                                                    self.spec.out_dtype.size)
+            return s
+
+    def _pick(self, vectors, n):
+        if self.vectorized is not None:
+            used = [(addr, local, p.dtype.size, self.access[p.name])
+                    for p, addr, local in vectors if self.access[p.name].used]
+            if cg.vector_path_ok(used, n):
+                return self.vectorized, self.variant.unroll * self.width
+        return self.generic, self.variant.unroll
+
+    def _read(self, address: int, dtype: Dtype):
+        from . import _runtime
+        box = nd.ctype_for(dtype)()
+        _runtime.memcpy_dtoh(ctypes.addressof(box), address, dtype.size)
+        _runtime.stream_synchronize()
+        return dtype.np.type(box.value)
+
+    def _launch_combine(self, partials: int, count: int, result: int, out: int,
+                        stream=None) -> None:
+        from . import _runtime
+        vals = [ctypes.c_uint64(partials), ctypes.c_uint64(result), ctypes.c_uint64(out),
+                ctypes.c_long(0), ctypes.c_long(count)]
+        _runtime.launch(self.combine.function(), 1, 32, cg.pack(vals), 0, stream)
+
+    def _check_neutral(self) -> None:
+        """fold([v]) must give v back for exactly representable samples
+        (``src/reduction.py:218-234``); runs the compiled combine on device."""
+        from . import _runtime
+        kind = self.spec.acc_dtype.kind
+        samples = {"f": [0.0, 1.5, -2.25, 7.0], "u": [0, 1, 7, 200]}.get(kind, [0, 1, -3, 99])
+        dev = _runtime.current_device()
+        s = self.scratch(dev)
+        s.ensure(1)
+        for value in samples:
+            box = self._acc_ctype(value)
+            _runtime.memcpy_htod(s.partials, ctypes.addressof(box), self.spec.acc_dtype.size)
+            self._launch_combine(s.partials, 1, s.result, s.out)
+            folded = self._read(s.result, self.spec.acc_dtype)
+            if folded != self.spec.acc_dtype.np.type(value):
+                raise ValueError(
+                    f"neutral {self.spec.neutral!r} is not an identity for "
+                    f"{self.spec.reduce_expr!r}: fold([{value!r}]) gave {folded!r}")
+
+    def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
+               out: nd.NdArray | None = None):
+        """Asynchronous stage 1+2.  Returns the scratch (result address holds
+        the accumulator, ``out`` -- or the scratch out slot -- the out-dtype
+        value).  Used by ``__call__`` and by the multi-GPU driver."""
+        from . import _runtime
+        if n is not None and n < 0:
+            raise nd.ShapeMismatch(f"n must be non-negative, got {n}")
+        values, vectors, n = _marshal(self.spec.signature, args, n, self.name, base)
+        dev = _runtime.current_device()
+        s = self.scratch(dev)
+        out_addr = out.address if out is not None else s.out
+        if n == 0:
+            s.ensure(1)
+            self._launch_combine(s.partials, 0, s.result, out_addr, stream)
+            return s
+        handle, per_thread = self._pick(vectors, n)
+        fn = handle.function(dev)
+        grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread)
+        s.ensure(grid)
+        values += [ctypes.c_long(base), ctypes.c_long(base + n), ctypes.c_uint64(s.partials),
+                   ctypes.c_uint64(s.result), ctypes.c_uint64(out_addr),
+                   ctypes.c_uint64(s.ticket)]
+        _runtime.launch(fn, grid, self.variant.block, cg.pack(values), 0, stream)
+        self.launches += 1
+        return s
+
+    def launch_config(self, *args, n: int | None = None) -> dict:
+        from . import _runtime
+        _, vectors, n = _marshal(self.spec.signature, args, n, self.name)
+        handle, per_thread = self._pick(vectors, n)
+        dev = _runtime.current_device()
+        grid = cg.grid_for(handle.function(dev), dev, self.variant.block,
+                           self.variant.workers, max(n, 1), per_thread)
+        return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n}
+
+    def __call__(self, *args, n: int | None = None, stream=None,
+                 return_device: bool | None = None, base: int = 0):
+        want_device = self.return_device if return_device is None else return_device
+        if want_device:
+            first = next(a for a, p in zip(args, self.spec.signature.params) if p.is_vector)
+            out = first.pool.alloc_uninitialized(self.spec.out_dtype, ())
+            self.launch(*args, n=n, base=base, stream=stream, out=out)
+            return out
+        s = self.launch(*args, n=n, base=base, stream=stream)
+        return self._read(s.out, self.spec.out_dtype)
+
+
+def make_reduction(signature, out_dtype, neutral: str, reduce_expr: str,
+                   map_expr: str | None = None, name: str = "reduce",
+                   variant: VariantParams | None = None, **kwargs) -> ReductionKernel:
+    """Reduction from the raw spec pieces (``src/reduction.py:261-268``)."""
+    spec = ReductionSpec(signature, nd.dtype_of(out_dtype), neutral, reduce_expr, map_expr)
+    return ReductionKernel(spec, name, variant, **kwargs)
+
+
+# --- stock reductions (src/reduction.py:273-312) -----------------------------------------------
+
+
+def _lowest(d: Dtype) -> str:
+    return {"i": f"INT{d.size * 8}_MIN", "u": "0", "f": "-INFINITY"}[d.kind]
+
+
+def _highest(d: Dtype) -> str:
+    return {"i": f"INT{d.size * 8}_MAX", "u": f"UINT{d.size * 8}_MAX", "f": "INFINITY"}[d.kind]
+
+
+def sum_kernel(dtype, variant: VariantParams | None = None, **kwargs) -> ReductionKernel:
+    d = nd.dtype_of(dtype)
+    return make_reduction(f"{d.cname} *x", d, "0", "a + b", name="sum_k",
+                          variant=variant, **kwargs)
+
+
+def max_kernel(dtype, variant: VariantParams | None = None, **kwargs) -> ReductionKernel:
+    d = nd.dtype_of(dtype)
+    return make_reduction(f"{d.cname} *x", d, _lowest(d), "a > b ? a : b", name="max_k",
+                          variant=variant, **kwargs)
+
+
+def min_kernel(dtype, variant: VariantParams | None = None, **kwargs) -> ReductionKernel:
+    d = nd.dtype_of(dtype)
+    return make_reduction(f"{d.cname} *x", d, _highest(d), "a < b ? a : b", name="min_k",
+                          variant=variant, **kwargs)
+
+
+def dot_kernel(dtype, variant: VariantParams | None = None, **kwargs) -> ReductionKernel:
+    """Inner product of two same-dtype vectors."""
+    d = nd.dtype_of(dtype)
+    return make_reduction(f"{d.cname} *x, {d.cname} *y", d, "0", "a + b",
+                          map_expr="x[i] * y[i]", name="dot_k", variant=variant, **kwargs)

@@ -1,0 +1,91 @@
+${prelude}
+// ---- reduction kernel "${name}" (templates/reduction.cu) --------------------
+// reduce_expr over a and b, and map_expr over the parameters and i, verbatim.
+// rtcg_fold(acc, map) is the reference's textual "acc = reduce(a->acc,
+// b->(map))" (src/reduction.py:98-103); rtcg_fold(acc, partial) is its
+// combine (src/reduction.py:154-156).  Accumulator: ${acc_t}.
+
+template <class rtcg_B>
+__device__ __forceinline__ ${acc_t} rtcg_fold(${acc_t} a, rtcg_B b)
+{
+    return (${reduce_expr});
+}
+
+template <${map_tparams}>
+__device__ __forceinline__ auto rtcg_map(const long i${map_params})
+{
+    return (${map_expr});
+}
+
+#define RTCG_NEUTRAL ((${acc_t})(${neutral}))
+
+// General path: thread-serial folds in index order, then lanes -> warps ->
+// CTA partial, then the last CTA folds the partials in CTA order.
+extern "C" __global__ void __launch_bounds__(${block})
+${name}_g(${kparams_generic}, const long start, const long end,
+    ${acc_t} *rtcg_partials, ${acc_t} *rtcg_result, ${out_t} *rtcg_out,
+    unsigned int *rtcg_ticket)
+{
+${unpack}
+    ${acc_t} acc = ${neutral};
+    const rtcg::span sp = rtcg::partition<rtcg::${chunking}>(start, end);
+    rtcg::for_each<${unroll}>(sp.lo + sp.first, sp.hi, sp.step, [&](const long i) {
+        acc = rtcg_fold(acc, rtcg_map<${ptr_types_generic}>(i${call_args}));
+    });
+    rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+}
+{% if vector %}
+// Vector path: ${unroll} x 16-byte chunks per vector per thread per step,
+// loaded before the fold chain consumes them.
+extern "C" __global__ void __launch_bounds__(${block})
+${name}(${kparams_vector}, const long start, const long end,
+    ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
+    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket)
+{
+${unpack}
+    constexpr int E = ${width};
+    constexpr int U = ${unroll};
+    ${acc_t} acc = ${neutral};
+    const rtcg::span sp = rtcg::partition<rtcg::${chunking}>(start, end);
+    const rtcg::tiles tl = rtcg::tile(sp.lo, sp.hi, E);
+    auto elem = [&](const long i) {
+        acc = rtcg_fold(acc, rtcg_map<${ptr_types_vector}>(i${call_args}));
+    };
+    rtcg::for_each<1>(sp.lo + sp.first, tl.head_hi, sp.step, elem);
+    rtcg::for_each<1>(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
+    for (long c = tl.c_lo + sp.first; c < tl.c_hi; c += U * sp.step) {
+${vec_decls}
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long cu = c + u * sp.step;
+            if (cu < tl.c_hi) {
+${vec_loads}
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long cu = c + u * sp.step;
+            if (cu < tl.c_hi) {
+#pragma unroll
+                for (int k = 0; k < E; ++k)
+                    acc = rtcg_fold(acc, rtcg_map<${lane_types}>(cu * E + k${lane_args}));
+            }
+        }
+    }
+    rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+}
+{% endif %}
+// Ordered fold of partials[start, end) from the neutral into result[0]; the
+// reference's <name>_combine entry point (src/reduction.py:154-168).  Used for
+// empty spans, the neutral probe and the cross-GPU combine of rank partials.
+extern "C" __global__ void ${name}_combine(const ${acc_t} *rtcg_in, ${acc_t} *rtcg_result,
+                                           ${out_t} *rtcg_out, const long start, const long end)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ${acc_t} acc = ${neutral};
+    for (long i = start; i < end; ++i) acc = rtcg_fold(acc, rtcg_in[i]);
+    rtcg_result[0] = acc;
+    rtcg_out[0] = (${out_t})acc;
+}

@@ -1,0 +1,205 @@
+"""GPU parity of generated reductions against the reference and the oracle.
+
+Bars (BASELINE.md §2 / SURVEY.md §8c):
+* integer reductions and max/min: bit-exact;
+* float sums with fp64 accumulation: |got - fsum(terms)| <=
+  1/2 ulp_out(result) + n * 2^-53 * sum|terms| (``oracle.csem.float_reduction_bound``),
+  plus bitwise reproducibility for a fixed variant.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import cport, csem
+from paper_0911_3456_b200 import elementwise as ew, ndarray as nd, reduction as rd
+
+pytestmark = pytest.mark.gpu
+
+_VARIANTS = (ew.VariantParams(), ew.VariantParams(unroll=1, block=64, workers=7),
+             ew.VariantParams(unroll=8, block=512, chunking="contiguous-blocks"),
+             ew.VariantParams(unroll=2, block=1024, workers=1))
+
+
+def test_reference_known_answers(kernel_env, golden):
+    kwargs, pool = kernel_env
+    assert rd.sum_kernel(nd.int32, **kwargs)(nd.from_host(pool, nd.int32, [1, 2, 3, 4])) == 10
+    x = nd.from_host(pool, nd.float64, [1.0, 2.0])
+    y = nd.from_host(pool, nd.float64, [3.0, 4.0])
+    v = rd.dot_kernel(nd.float64, **kwargs)(x, y)
+    assert v == 11.0 and isinstance(v, np.float64)
+    assert rd.max_kernel(nd.float64, **kwargs)(pool.alloc(nd.float64, (0,))) == -np.inf
+    assert rd.sum_kernel(nd.uint16, **kwargs)(pool.alloc(nd.uint16, (0,))) == 0
+    i8 = nd.from_host(pool, nd.int8, [-128, 5, 127, -1])
+    assert rd.max_kernel(nd.int8, **kwargs)(i8) == 127
+    assert rd.min_kernel(nd.int8, **kwargs)(i8) == -128
+    s16 = rd.sum_kernel(nd.int16, **kwargs)(nd.from_host(pool, nd.int16, [1, 2, 3]))
+    assert s16.dtype == np.int16 and s16 == 6
+    assert rd.sum_kernel(nd.int32, **kwargs)(nd.from_host(pool, nd.int32, [10, 20, 30, 40]),
+                                             n=2) == 30
+    cnt = rd.make_reduction("float t, float *x", nd.float32, "0", "a + b",
+                            map_expr="(x[i] > t) ? 1.0f : 0.0f", name="count_above", **kwargs)
+    assert cnt(0.6, nd.from_host(pool, nd.float32, [0.1, 0.9, 0.5, 0.7])) == 2.0
+
+
+def test_int32_and_f32_folds_vs_reference_goldens(kernel_env, golden):
+    kwargs, pool = kernel_env
+    r = golden["reductions"]
+    d = np.random.default_rng(7)
+    ints = d.integers(-100, 101, size=5000).astype(np.int32)
+    ai = nd.from_host(pool, nd.int32, ints)
+    for v in _VARIANTS:
+        got = [int(rd.sum_kernel(nd.int32, v, **kwargs)(ai)),
+               int(rd.max_kernel(nd.int32, v, **kwargs)(ai)),
+               int(rd.min_kernel(nd.int32, v, **kwargs)(ai))]
+        assert got == r["int32_sum_max_min_seed7"], v
+    floats = d.uniform(0.0, 1.0, size=10**6).astype(np.float32)
+    af = nd.from_host(pool, nd.float32, floats)
+    bound = csem.float_reduction_bound(floats, "float32")
+    exact = csem.exact_sum(floats)
+    for v in _VARIANTS:
+        got = float(rd.sum_kernel(nd.float32, v, **kwargs)(af))
+        assert abs(got - exact) <= bound
+        assert abs(got - r["f32_sum_1e6_seed7_after_ints"]) / exact <= 1e-6
+
+
+def test_int64_variants_exact(kernel_env, golden):
+    kwargs, pool = kernel_env
+    want = golden["reductions"]["int64_1003_seed11_sum_max_min"]
+    host = np.random.default_rng(11).integers(-120, 120, size=1003, dtype=np.int64)
+    x = nd.from_host(pool, nd.int64, host)
+    for v in _VARIANTS:
+        assert [int(rd.sum_kernel(nd.int64, v, **kwargs)(x)),
+                int(rd.max_kernel(nd.int64, v, **kwargs)(x)),
+                int(rd.min_kernel(nd.int64, v, **kwargs)(x))] == want
+
+
+def test_wrapping_int64_sum_bit_exact(kernel_env, golden):
+    """C4's int64 sum: values in [-2^62, 2^62) wrap; order independent."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(1)
+    big = rng.integers(-(1 << 62), 1 << 62, size=1 << 20, dtype=np.int64)
+    x = nd.from_host(pool, nd.int64, big)
+    for v in _VARIANTS:
+        assert int(rd.sum_kernel(nd.int64, v, **kwargs)(x)) == \
+            golden["reductions"]["sum_i64_2p20_seed1"]
+
+
+def test_dot_f32_vs_reference(kernel_env, golden):
+    kwargs, pool = kernel_env
+    for n, seed, key in ((1 << 20, 0, "dot_f32_2p20_seed0"), (1000, 3, "dot_f32_1000_seed3")):
+        rng = np.random.default_rng(seed)
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        y = rng.uniform(-1, 1, n).astype(np.float32)
+        gx, gy = nd.from_host(pool, nd.float32, x), nd.from_host(pool, nd.float32, y)
+        terms = (x * y).astype(np.float64)   # products rounded in fp32, as in C
+        bound = csem.float_reduction_bound(terms, "float32")
+        exact = csem.exact_sum(terms)
+        ref = golden["reductions"][key]
+        equal = 0
+        for v in _VARIANTS:
+            got = float(rd.dot_kernel(nd.float32, v, **kwargs)(gx, gy))
+            assert abs(got - exact) <= bound, (v, got, exact)
+            equal += got == ref
+        assert equal >= len(_VARIANTS) - 1  # fp64 accumulation: ties aside, bit-equal
+
+
+def test_maxabs_and_sumsq_c4_expressions(kernel_env, golden):
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(1)
+    g = rng.standard_normal(1 << 20).astype(np.float32)
+    ag = nd.from_host(pool, nd.float32, g)
+    mx = rd.make_reduction("float *x", nd.float32, "0", "a > b ? a : b", "fabsf(x[i])",
+                           name="maxabs", **kwargs)
+    assert float(mx(ag)) == golden["reductions"]["maxabs_f32_2p20_seed1"]
+    sq = rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i] * x[i]",
+                           name="sumsq", **kwargs)
+    terms = (g * g).astype(np.float64)
+    got = float(sq(ag))
+    assert abs(got - csem.exact_sum(terms)) <= csem.float_reduction_bound(terms, "float32")
+    assert abs(got - golden["reductions"]["sumsq_f32_2p20_seed1"]) <= \
+        csem.float_reduction_bound(terms, "float32")
+
+
+@pytest.mark.parametrize("dname", csem.DTYPE_NAMES)
+def test_every_dtype_sum_max_min_vs_c_port(kernel_env, dname):
+    kwargs, pool = kernel_env
+    d = nd.BY_NAME[dname]
+    rng = np.random.default_rng(17)
+    n = 123_457
+    host = (rng.uniform(-50, 50, n) if d.kind == "f" else
+            rng.integers(0 if d.kind == "u" else -50, 50, n)).astype(d.np)
+    x = nd.from_host(pool, d, host)
+    for kind, neutral, expr in (("sum", "0", "a + b"),
+                                ("max", rd._lowest(d), "a > b ? a : b"),
+                                ("min", rd._highest(d), "a < b ? a : b")):
+        got = rd.make_reduction(f"{d.cname} *x", d, neutral, expr, name=f"{kind}_{dname}",
+                                **kwargs)(x)
+        want = cport.Reduction(f"{d.cname} *x", dname, neutral, expr)(host, workers=4)
+        if d.kind == "f" and kind == "sum":
+            terms = host.astype(np.float64)
+            assert abs(float(got) - csem.exact_sum(terms)) <= \
+                csem.float_reduction_bound(terms, dname)
+        else:
+            assert got == want and got.dtype == want.dtype, (kind, got, want)
+
+
+def test_float_sum_bitwise_reproducible(kernel_env):
+    kwargs, pool = kernel_env
+    host = np.random.default_rng(9).uniform(-1, 1, 1_000_003).astype(np.float32)
+    x = nd.from_host(pool, nd.float32, host)
+    for v in _VARIANTS:
+        k = rd.sum_kernel(nd.float32, v, **kwargs)
+        first = k(x)
+        assert all(k(x) == first for _ in range(5))
+
+
+def test_general_path_reduction_with_neighbour_access(kernel_env):
+    kwargs, pool = kernel_env
+    n = 50_001
+    host = np.random.default_rng(3).uniform(-1, 1, n + 1)
+    x = nd.from_host(pool, nd.float64, host)
+    k = rd.make_reduction("double *x", nd.float64, "0", "a + b", "x[i+1] - x[i]",
+                          name="tv", **kwargs)
+    assert k.vectorized is None
+    terms = np.diff(host)
+    got = float(k(x, n=n))
+    assert abs(got - csem.exact_sum(terms)) <= csem.float_reduction_bound(terms, "float64")
+
+
+def test_neutral_probe(kernel_env):
+    kwargs, pool = kernel_env
+    with pytest.raises(ValueError):
+        rd.make_reduction("int32_t *x", nd.int32, "7", "a + b", name="bad_neutral",
+                          debug=True, **kwargs)
+    k = rd.make_reduction("int32_t *x", nd.int32, "0", "a + b", name="good_neutral",
+                          debug=True, **kwargs)
+    assert k(nd.from_host(pool, nd.int32, [4, 5])) == 9
+
+
+def test_pycuda_constructor_returns_device_scalar(kernel_env):
+    kwargs, pool = kernel_env
+    k = rd.ReductionKernel(np.float32, neutral="0", reduce_expr="a+b",
+                           map_expr="x[i]*y[i]", arguments="float *x, float *y",
+                           cache=kwargs["cache"], config=kwargs["config"])
+    x = nd.from_host(pool, nd.float32, [1.0, 2.0, 3.0])
+    y = nd.from_host(pool, nd.float32, [4.0, 5.0, 6.0])
+    out = k(x, y)
+    assert isinstance(out, nd.NdArray) and out.shape == () and out.get() == 32.0
+    assert k(x, y, return_device=False) == np.float32(32.0)
+
+
+def test_large_reduction_properties(kernel_env):
+    """2^27 elements: dot(x, 1) == sum(x) bitwise for integers; float dot vs bound."""
+    kwargs, pool = kernel_env
+    n = 1 << 27
+    rng = np.random.default_rng(21)
+    xi = rng.integers(-1000, 1000, n, dtype=np.int64)
+    ones = np.ones(n, np.int64)
+    gx, go = nd.from_host(pool, nd.int64, xi), nd.from_host(pool, nd.int64, ones)
+    assert int(rd.dot_kernel(nd.int64, **kwargs)(gx, go)) == int(xi.sum())
+    assert int(rd.sum_kernel(nd.int64, **kwargs)(gx)) == int(xi.sum())
+    xf = rng.uniform(-1, 1, n).astype(np.float32)
+    gf = nd.from_host(pool, nd.float32, xf)
+    got = float(rd.dot_kernel(nd.float32, **kwargs)(gf, gf))
+    terms = (xf * xf).astype(np.float64)
+    assert abs(got - float(np.sum(terms))) <= csem.float_reduction_bound(terms, "float32")
