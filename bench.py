@@ -159,36 +159,48 @@ class Dist:
 # --- CPU reference ---------------------------------------------------------------------------------
 
 
-def cpu_reference(workload: str, budget_s: float = 12.0, n_sample: int = 1 << 26):
-    """Time the reference CPU kernel on a bounded sample; returns a dict."""
+def cpu_reference(workload: str, steps: int | None = None, warmup: int = 1,
+                  budget_s: float = 10.0, n_sample: int = 1 << 26):
+    """Time the reference CPU kernel on a bounded sample of the workload.
+
+    ``steps`` given: exactly that many timed calls after ``warmup`` (mean);
+    else calls until ``budget_s`` (>= 3, <= 50; best).  Returns a dict."""
     from oracle import refdrive
     fn, kind = refdrive.load(workload)
     threads = refdrive.host_threads()
     rng = np.random.default_rng(0)
     x = rng.uniform(-1, 1, n_sample).astype(np.float32)
     y = rng.uniform(-1, 1, n_sample).astype(np.float32)
-    fn(x, y, workers=threads)  # warm (page in, thread spin-up)
-    times, t_end = [], time.perf_counter() + budget_s
-    while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
+    for _ in range(max(1, warmup)):
+        fn(x, y, workers=threads)  # page in, thread spin-up
+    times = []
+    if steps is not None:
         t0 = time.perf_counter()
-        fn(x, y, workers=threads)
-        times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": round(8 * n_sample / best / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "kind": kind, "seconds_per_call": best, "calls": len(times),
-            "sample": f"dot f32 n=2^{int(math.log2(n_sample))} (of the 2^28 workload), "
-                      f"x,y~U(-1,1) seed 0, reference variant unroll=4 contiguous, "
-                      f"{threads} worker threads, best of {len(times)} calls"}
+        for _ in range(steps):
+            fn(x, y, workers=threads)
+        per_call, stat = (time.perf_counter() - t0) / steps, f"mean of {steps} calls"
+    else:
+        t_end = time.perf_counter() + budget_s
+        while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
+            t0 = time.perf_counter()
+            fn(x, y, workers=threads)
+            times.append(time.perf_counter() - t0)
+        per_call, stat = min(times), f"best of {len(times)} calls"
+    return {"value": round(8 * n_sample / per_call / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": kind, "seconds_per_call": per_call,
+            "calls": steps if steps is not None else len(times),
+            "sample": f"dot f32 n=2^{int(math.log2(n_sample))} per call (bounded sample of the "
+                      f"2^28 workload), x,y~U(-1,1) seed 0, reference variant unroll=4 "
+                      f"contiguous-blocks, {threads} worker threads, {stat}"}
 
 
 def run_reference(args) -> int:
-    d = Dist(args.gpus)
-    if d.rank != 0:
-        d.close()
+    """CPU reference arm: rank 0 only, no GPU or process group needed."""
+    if _env_int("RANK", 0) != 0:
         return 0
-    base = cpu_reference("dot_k", budget_s=max(3.0, 0.5 * args.steps))
+    base = cpu_reference("dot_k", steps=args.steps, warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s",
-            "n_gpus": args.gpus, "steps": base["calls"], "warmup": 1,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(base["seconds_per_call"] * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": WORKLOAD + " (CPU: bounded sample)",
@@ -197,7 +209,6 @@ def run_reference(args) -> int:
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
-    d.close()
     return 0
 
 
@@ -248,9 +259,7 @@ def run_ours(args) -> int:
         # autotune block x unroll for (dot, float32, n) -- outside the timed region
         spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
         t0 = time.perf_counter()
-        tuned = at.tune_reduction(spec, "dot_k", n, {"unroll": (1, 2, 4, 8),
-                                                     "block": (128, 256, 512, 1024)},
-                                  args=[gx, gy],
+        tuned = at.tune_reduction(spec, "dot_k", n, at.DEFAULT_AXES, args=[gx, gy],
                                   protocol=at.MeasurementProtocol(warmup=2, repeats=5),
                                   store=at.TuneStore())
         tune_s = time.perf_counter() - t0
@@ -303,7 +312,8 @@ def run_ours(args) -> int:
         gx2.free()
         gy2.free()
 
-        workloads = {} if args.quick or d.world > 1 else secondary_workloads(rt, nd, ew, rd, pool, peak)
+        workloads = {} if args.quick or d.world > 1 else \
+            secondary_workloads(rt, nd, ew, rd, at, pool, peak)
 
     algo_bytes = 8 * n
     achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
@@ -357,11 +367,14 @@ def _ncu_traffic(kernel: str):
         return None
 
 
-def secondary_workloads(rt, nd, ew, rd, pool, peak):
-    """The other BASELINE configs, single GPU, device-timed (best of 10)."""
+def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
+    """The other BASELINE configs on one GPU: each kernel autotuned over
+    unroll x block (TuneStore-cached), then device-timed (best of 10)."""
     out = {}
     n = N_PER_GPU
     rng = np.random.default_rng(1)
+    proto = at.MeasurementProtocol(warmup=1, repeats=3)
+    store = at.TuneStore()
 
     def best_ms(fn, reps=10):
         fn()
@@ -372,38 +385,50 @@ def secondary_workloads(rt, nd, ew, rd, pool, peak):
             best = min(best, ms)
         return best
 
-    def record(name, fn, nbytes, **extra):
+    def record(name, fn, nbytes, tuned, **extra):
         ms = best_ms(fn)
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
-                     "algorithmic_bytes": nbytes, **extra}
+                     "algorithmic_bytes": nbytes, "variant": tuned.best_assignment,
+                     "tune_from_store": tuned.from_store, **extra}
 
     x = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
     y = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
     z = pool.alloc_uninitialized(nd.float32, (n,))
-    axpy = ew.ElementwiseKernel("float a, float *x, float b, float *y, float *z",
-                                "z[i] = a * x[i] + b * y[i]", "axpy")
-    record("axpy_f32_2p28", lambda: axpy(2.0, x, -3.0, y, z), 12 * n,
-           variant=str(axpy.variant))
+    sig, op = "float a, float *x, float b, float *y, float *z", "z[i] = a * x[i] + b * y[i]"
+    t = at.tune_elementwise(sig, op, "axpy", n, at.DEFAULT_AXES, args=[2.0, x, -3.0, y, z],
+                            protocol=proto, store=store)
+    axpy = ew.ElementwiseKernel(sig, op, "axpy", ew.VariantParams(**t.best_assignment))
+    record("axpy_f32_2p28", lambda: axpy(2.0, x, -3.0, y, z), 12 * n, t)
     o32 = pool.alloc_uninitialized(nd.float32, ())
-    mx = rd.make_reduction("float *x", nd.float32, "0", "a > b ? a : b", "fabsf(x[i])",
-                           name="maxabs")
-    record("maxabs_f32_2p28", lambda: mx.launch(x, out=o32), 4 * n)
-    sq = rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i] * x[i]", name="sumsq")
-    record("l2sq_f32_2p28", lambda: sq.launch(x, out=o32), 4 * n)
+    for name, mp, red in (("maxabs", "fabsf(x[i])", "a > b ? a : b"),
+                          ("sumsq", "x[i] * x[i]", "a + b")):
+        spec = rd.ReductionSpec("float *x", nd.float32, "0", red, mp)
+        t = at.tune_reduction(spec, name, n, at.DEFAULT_AXES, args=[x], protocol=proto,
+                              store=store)
+        k = rd.ReductionKernel(spec, name, ew.VariantParams(**t.best_assignment))
+        record(f"{name}_f32_2p28", lambda: k.launch(x, out=o32), 4 * n, t,
+               note="L2 norm = sqrt of sumsq (host)" if name == "sumsq" else "max|x|")
     for a in (x, y, z):
         a.free()
     xd = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
     zd = pool.alloc_uninitialized(nd.float64, (n,))
-    ps = ew.ElementwiseKernel("double a, double *x, double *z",
-                              "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])", "polysin")
-    record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n)
+    sig, op = ("double a, double *x, double *z",
+               "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
+    t = at.tune_elementwise(sig, op, "polysin", n, at.DEFAULT_AXES, args=[0.5, xd, zd],
+                            protocol=proto, store=store)
+    ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**t.best_assignment))
+    record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n, t,
+           bound="fp64 issue (double sin: ~37 DP instructions/element), not HBM")
     xd.free()
     zd.free()
     xi = nd.from_host(pool, nd.int64, rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64))
     o64 = pool.alloc_uninitialized(nd.int64, ())
-    si = rd.sum_kernel(nd.int64)
-    record("sum_i64_2p28", lambda: si.launch(xi, out=o64), 8 * n)
+    spec = rd.ReductionSpec("int64_t *x", nd.int64, "0", "a + b")
+    t = at.tune_reduction(spec, "sum_k", n, at.DEFAULT_AXES, args=[xi], protocol=proto,
+                          store=store)
+    si = rd.ReductionKernel(spec, "sum_k", ew.VariantParams(**t.best_assignment))
+    record("sum_i64_2p28", lambda: si.launch(xi, out=o64), 8 * n, t)
     xi.free()
     return out
 
