@@ -23,10 +23,13 @@ from __future__ import annotations
 import ctypes
 import math
 import re
+import struct
+import threading
 from dataclasses import dataclass
 from functools import lru_cache
 from pathlib import Path
 
+from . import _runtime
 from . import csyntax as cs
 
 TEMPLATES = Path(__file__).resolve().parent / "templates"
@@ -185,6 +188,80 @@ def scalar_value(value, dtype):
     return ctypes.c_int64(int(value))
 
 
+_MASK64 = (1 << 64) - 1
+_PACK_D = struct.Struct("<d").pack
+_UNPACK_Q = struct.Struct("<Q").unpack
+
+
+def _bits(value, kind: str) -> int:
+    """The 8 bytes of the widened scalar slot, as an unsigned integer."""
+    if kind == "f":
+        return _UNPACK_Q(_PACK_D(float(value)))[0]
+    return int(value) & _MASK64
+
+
+class Binder:
+    """Argument marshalling for one kernel signature into preallocated
+    per-thread parameter slots (every kernel parameter is 8 bytes: pointers,
+    widened scalars, ``long start/end``, scratch pointers).  cuLaunchKernel
+    copies parameter values at launch, so the slots are reusable as soon as
+    the launch call returns.  Validation follows ``src/elementwise.py:324-366``.
+    """
+
+    def __init__(self, sig, extra: int = 0) -> None:
+        self.params = sig.params
+        self.count = len(self.params)
+        self.total = self.count + 2 + extra
+        self._tls = threading.local()
+
+    def slots(self):
+        held = getattr(self._tls, "slots", None)
+        if held is None:
+            vals = (ctypes.c_uint64 * self.total)()
+            base = ctypes.addressof(vals)
+            ptrs = (ctypes.c_void_p * self.total)(*[base + 8 * k for k in range(self.total)])
+            held = self._tls.slots = (vals, ptrs)
+        return held
+
+    def bind(self, args, n, base: int, name: str, errors):
+        """-> (vals, ptrs, vectors, n); ``vectors`` = [(param, addr0, local)].
+        ``errors`` = (ArityMismatch, DtypeMismatch, ShapeMismatch, NdArray)."""
+        arity, dtype_err, shape_err, array_t = errors
+        params = self.params
+        if len(args) != self.count:
+            raise arity(f"kernel {name} takes {self.count} arguments, got {len(args)}")
+        vals, ptrs = self.slots()
+        vectors = []
+        for k, p in enumerate(params):
+            arg = args[k]
+            if p.is_vector:
+                if not isinstance(arg, array_t):
+                    raise dtype_err(p.name, f"expected a GPUArray, got {type(arg).__name__}")
+                if arg.dtype is not p.dtype and arg.dtype != p.dtype:
+                    raise dtype_err(p.name, f"expected dtype {p.dtype.name}, "
+                                            f"got {arg.dtype.name}")
+                if n is None:
+                    n = arg.size
+                if arg.size < n:
+                    raise shape_err(f"vector {p.name!r} holds {arg.size} elements, "
+                                    f"kernel span is {n}")
+                local = arg.address
+                addr0 = (local - base * p.dtype.size) & _MASK64
+                vals[k] = addr0
+                vectors.append((p, addr0, local))
+            else:
+                if isinstance(arg, array_t):
+                    raise dtype_err(p.name, "expected a scalar, got a GPUArray")
+                vals[k] = _bits(arg, p.dtype.kind)
+        if n is None:
+            raise arity("cannot infer n: no vector arguments")
+        return vals, ptrs, vectors, n
+
+    def set_range(self, vals, start: int, end: int) -> None:
+        vals[self.count] = start & _MASK64
+        vals[self.count + 1] = end & _MASK64
+
+
 def pack(values) -> ctypes.Array:
     """cuLaunchKernel parameter array: pointers to each ctypes value."""
     arr = (ctypes.c_void_p * len(values))()
@@ -197,16 +274,17 @@ def vector_path_ok(entries, n: int) -> bool:
     """entries: (index-0 address, local address, itemsize, Access) per used
     vector.  True when every index-0 address is 16-byte aligned and no written
     vector overlaps another used vector over the n local elements."""
-    spans = []
-    for addr0, local, size, acc in entries:
-        if addr0 % 16:
-            return False
-        spans.append((local, local + n * size, acc.written))
-    for a in range(len(spans)):
-        lo_a, hi_a, w_a = spans[a]
-        for b in range(a + 1, len(spans)):
-            lo_b, hi_b, w_b = spans[b]
-            if (w_a or w_b) and lo_a < hi_b and lo_b < hi_a:
+    bits = 0
+    for e in entries:
+        bits |= e[0]
+    if bits & 15:
+        return False
+    for a, (_, lo_a, size_a, acc_a) in enumerate(entries):
+        if not acc_a.written:
+            continue
+        hi_a = lo_a + n * size_a
+        for b, (_, lo_b, size_b, _acc) in enumerate(entries):
+            if b != a and lo_a < lo_b + n * size_b and lo_b < hi_a:
                 return False
     return True
 
@@ -217,17 +295,29 @@ _sm_count: dict[int, int] = {}
 def sm_count(device: int) -> int:
     hit = _sm_count.get(device)
     if hit is None:
-        from . import _runtime
         hit = _sm_count[device] = _runtime.device_info(device)["sm_count"]
     return hit
+
+
+_grid_cache: dict = {}
 
 
 def grid_for(function: int, device: int, block: int, workers: int | None,
              n: int, per_thread: int) -> int:
     """CTAs to launch: explicit ``workers``, else enough resident CTAs to
     fill every SM once (persistent-style), never more than the work needs."""
-    from . import _runtime
-    useful = max(1, math.ceil(n / (block * per_thread)))
+    key = (function, device, block, workers, n, per_thread)
+    hit = _grid_cache.get(key)
+    if hit is not None:
+        return hit
+    if len(_grid_cache) > 4096:
+        _grid_cache.clear()
+    grid = _grid_cache[key] = _compute_grid(function, device, block, workers, n, per_thread)
+    return grid
+
+
+def _compute_grid(function, device, block, workers, n, per_thread) -> int:
+    useful = max(1, -(-n // (block * per_thread)))
     if workers is not None:
         grid = workers
     else:

@@ -24,6 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _runtime
 from . import ndarray as nd
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
@@ -125,7 +126,6 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False):
     All three run in stream order on torch's current stream.
     """
     import torch
-    from . import _runtime
 
     local_args, base = _locals(args)
     n_local = next(a.size for a in local_args if isinstance(a, nd.NdArray))

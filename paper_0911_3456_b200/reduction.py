@@ -35,10 +35,11 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _runtime
 from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
-from .elementwise import (KernelSignature, ParseError, VariantParams, _CHUNK_TOKEN,
+from .elementwise import (_CHUNK_TOKEN, _ERRORS, KernelSignature, ParseError, VariantParams,
                           _check_name, _marshal, parse_signature)
 from .ndarray import Dtype
 
@@ -117,7 +118,6 @@ class _Scratch:
     """Per-device partials / result / out / ticket buffers of one kernel."""
 
     def __init__(self, acc_size: int, out_size: int) -> None:
-        from . import _runtime
         self.capacity = 0
         self.partials = 0
         self.acc_size, self.out_size = acc_size, out_size
@@ -127,7 +127,6 @@ class _Scratch:
         _runtime.memset_async(self.result, 0, 64)
 
     def ensure(self, count: int) -> None:
-        from . import _runtime
         if count > self.capacity:
             if self.partials:
                 _runtime.synchronize()
@@ -194,6 +193,7 @@ class ReductionKernel:
         self.vectorized = jit.get_kernel(self.module, name) if self.access and self.width else None
         self.combine = jit.get_kernel(self.module, f"{name}_combine")
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
+        self._binder = cg.Binder(sig, extra=4)
         self._scratch: dict[int, _Scratch] = {}
         self._lock = threading.Lock()
         self.launches = 0
@@ -223,7 +223,6 @@ class ReductionKernel:
         return self.generic, self.variant.unroll
 
     def _read(self, address: int, dtype: Dtype):
-        from . import _runtime
         box = nd.ctype_for(dtype)()
         _runtime.memcpy_dtoh(ctypes.addressof(box), address, dtype.size)
         _runtime.stream_synchronize()
@@ -231,7 +230,6 @@ class ReductionKernel:
 
     def _launch_combine(self, partials: int, count: int, result: int, out: int,
                         stream=None) -> None:
-        from . import _runtime
         vals = [ctypes.c_uint64(partials), ctypes.c_uint64(result), ctypes.c_uint64(out),
                 ctypes.c_long(0), ctypes.c_long(count)]
         _runtime.launch(self.combine.function(), 1, 32, cg.pack(vals), 0, stream)
@@ -239,7 +237,6 @@ class ReductionKernel:
     def _check_neutral(self) -> None:
         """fold([v]) must give v back for exactly representable samples
         (``src/reduction.py:218-234``); runs the compiled combine on device."""
-        from . import _runtime
         kind = self.spec.acc_dtype.kind
         samples = {"f": [0.0, 1.5, -2.25, 7.0], "u": [0, 1, 7, 200]}.get(kind, [0, 1, -3, 99])
         dev = _runtime.current_device()
@@ -260,10 +257,9 @@ class ReductionKernel:
         """Asynchronous stage 1+2.  Returns the scratch (result address holds
         the accumulator, ``out`` -- or the scratch out slot -- the out-dtype
         value).  Used by ``__call__`` and by the multi-GPU driver."""
-        from . import _runtime
         if n is not None and n < 0:
             raise nd.ShapeMismatch(f"n must be non-negative, got {n}")
-        values, vectors, n = _marshal(self.spec.signature, args, n, self.name, base)
+        vals, ptrs, vectors, n = self._binder.bind(args, n, base, self.name, _ERRORS)
         dev = _runtime.current_device()
         s = self.scratch(dev)
         out_addr = out.address if out is not None else s.out
@@ -275,15 +271,17 @@ class ReductionKernel:
         fn = handle.function(dev)
         grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread)
         s.ensure(grid)
-        values += [ctypes.c_long(base), ctypes.c_long(base + n), ctypes.c_uint64(s.partials),
-                   ctypes.c_uint64(s.result), ctypes.c_uint64(out_addr),
-                   ctypes.c_uint64(s.ticket)]
-        _runtime.launch(fn, grid, self.variant.block, cg.pack(values), 0, stream)
+        b = self._binder
+        b.set_range(vals, base, base + n)
+        vals[b.count + 2] = s.partials
+        vals[b.count + 3] = s.result
+        vals[b.count + 4] = out_addr
+        vals[b.count + 5] = s.ticket
+        _runtime.launch(fn, grid, self.variant.block, ptrs, 0, stream)
         self.launches += 1
         return s
 
     def launch_config(self, *args, n: int | None = None) -> dict:
-        from . import _runtime
         _, vectors, n = _marshal(self.spec.signature, args, n, self.name)
         handle, per_thread = self._pick(vectors, n)
         dev = _runtime.current_device()
