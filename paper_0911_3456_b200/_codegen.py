@@ -303,24 +303,28 @@ _grid_cache: dict = {}
 
 
 def grid_for(function: int, device: int, block: int, workers: int | None,
-             n: int, per_thread: int) -> int:
-    """CTAs to launch: explicit ``workers``, else enough resident CTAs to
-    fill every SM once (persistent-style), never more than the work needs."""
-    key = (function, device, block, workers, n, per_thread)
+             n: int, per_thread: int, waves: int = 1) -> int:
+    """CTAs to launch: explicit ``workers``; else ``waves`` x the resident CTAs
+    (SMs x occupancy), never more than the work needs; ``waves=0`` = exactly
+    the work (one step per thread)."""
+    key = (function, device, block, workers, n, per_thread, waves)
     hit = _grid_cache.get(key)
     if hit is not None:
         return hit
     if len(_grid_cache) > 4096:
         _grid_cache.clear()
-    grid = _grid_cache[key] = _compute_grid(function, device, block, workers, n, per_thread)
+    grid = _grid_cache[key] = _compute_grid(function, device, block, workers, n, per_thread,
+                                            waves)
     return grid
 
 
-def _compute_grid(function, device, block, workers, n, per_thread) -> int:
+def _compute_grid(function, device, block, workers, n, per_thread, waves) -> int:
     useful = max(1, -(-n // (block * per_thread)))
     if workers is not None:
         grid = workers
+    elif waves == 0:
+        grid = useful
     else:
         resident = sm_count(device) * max(1, _runtime.occupancy(function, block))
-        grid = min(resident, useful)
+        grid = min(resident * waves, useful)
     return max(1, min(grid, 2**31 - 1))

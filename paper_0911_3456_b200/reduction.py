@@ -194,6 +194,7 @@ class ReductionKernel:
         self.combine = jit.get_kernel(self.module, f"{name}_combine")
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
         self._binder = cg.Binder(sig, extra=4)
+        self._waves = 1 if self.variant.waves is None else self.variant.waves
         self._scratch: dict[int, _Scratch] = {}
         self._lock = threading.Lock()
         self.launches = 0
@@ -269,7 +270,8 @@ class ReductionKernel:
             return s
         handle, per_thread = self._pick(vectors, n)
         fn = handle.function(dev)
-        grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread)
+        grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
+                           self._waves)
         s.ensure(grid)
         b = self._binder
         b.set_range(vals, base, base + n)
@@ -286,7 +288,7 @@ class ReductionKernel:
         handle, per_thread = self._pick(vectors, n)
         dev = _runtime.current_device()
         grid = cg.grid_for(handle.function(dev), dev, self.variant.block,
-                           self.variant.workers, max(n, 1), per_thread)
+                           self.variant.workers, max(n, 1), per_thread, self._waves)
         return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n}
 
     def __call__(self, *args, n: int | None = None, stream=None,
