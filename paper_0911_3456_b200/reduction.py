@@ -207,12 +207,15 @@ class ReductionKernel:
 
     # -- plumbing --
 
-    def scratch(self, device: int) -> _Scratch:
+    def scratch(self, device: int, stream: int | None = None) -> _Scratch:
+        """Partials / result / ticket buffers for (device, stream): launches on
+        different streams never share a ticket."""
+        key = (device, _runtime.current_stream() if stream is None else stream)
         with self._lock:
-            s = self._scratch.get(device)
+            s = self._scratch.get(key)
             if s is None:
-                s = self._scratch[device] = _Scratch(self.spec.acc_dtype.size,
-                                                    self.spec.out_dtype.size)
+                s = self._scratch[key] = _Scratch(self.spec.acc_dtype.size,
+                                                 self.spec.out_dtype.size)
             return s
 
     def _pick(self, vectors, n):
@@ -262,7 +265,7 @@ class ReductionKernel:
             raise nd.ShapeMismatch(f"n must be non-negative, got {n}")
         vals, ptrs, vectors, n = self._binder.bind(args, n, base, self.name, _ERRORS)
         dev = _runtime.current_device()
-        s = self.scratch(dev)
+        s = self.scratch(dev, stream)
         out_addr = out.address if out is not None else s.out
         if n == 0:
             s.ensure(1)

@@ -201,3 +201,21 @@ def test_array_metadata_and_interface():
     cai = a.__cuda_array_interface__
     assert cai["shape"] == (3, 5) and cai["typestr"] == "<i2" and cai["data"][0] == a.address
     assert nd.GPUArray is nd.NdArray and "GPUArray" in repr(a)
+
+
+def test_dropped_arrays_return_to_the_pool():
+    import gc
+    dev = HostDevice()
+    pool = dev.pool()
+    a = pool.alloc(nd.float32, (1000,))
+    held_before = pool.stats()["bytes_held"]
+    del a
+    gc.collect()
+    s = pool.stats()
+    assert s["bytes_held"] == held_before + 4096 and s["bytes_outstanding"] == 0
+    b = pool.alloc(nd.float32, (1000,))
+    assert pool.stats()["pool_hits"] == 1
+    pool.free(b)           # explicit free detaches the finalizer: no double return
+    del b
+    gc.collect()
+    assert pool.stats()["bytes_held"] == 4096

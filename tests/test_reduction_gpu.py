@@ -203,3 +203,37 @@ def test_large_reduction_properties(kernel_env):
     got = float(rd.dot_kernel(nd.float32, **kwargs)(gf, gf))
     terms = (xf * xf).astype(np.float64)
     assert abs(got - float(np.sum(terms))) <= csem.float_reduction_bound(terms, "float32")
+
+
+def test_c4_full_size_closed_forms(kernel_env):
+    """BASELINE C4 sizes (n = 2^32) through size-independent properties with
+    closed-form answers: inputs are generated on the device from i, and every
+    checked value is exactly representable, so the bar stays bit-exact."""
+    kwargs, pool = kernel_env
+    n = 1 << 32
+    xi = pool.alloc_uninitialized(nd.int64, (n,))
+    ew.ElementwiseKernel("long *x", "x[i] = i", "iota64", **kwargs)(xi)
+    s = int(rd.sum_kernel(nd.int64, **kwargs)(xi))
+    assert s == (n * (n - 1) // 2 + 2**63) % 2**64 - 2**63
+    assert int(rd.max_kernel(nd.int64, **kwargs)(xi)) == n - 1
+    assert int(rd.min_kernel(nd.int64, **kwargs)(xi)) == 0
+    xi.free()
+    xf = pool.alloc_uninitialized(nd.float32, (n,))
+    ew.ElementwiseKernel("float *x", "x[i] = (float) (i % 1024) - 511.0f", "saw",
+                         **kwargs)(xf)
+    block = np.arange(1024, dtype=np.float64) - 511.0
+    reps = n // 1024
+    mx = rd.make_reduction("float *x", nd.float32, "0", "a > b ? a : b", "fabsf(x[i])",
+                           name="maxabs_c4", **kwargs)
+    assert float(mx(xf)) == 512.0
+    sq = rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i] * x[i]",
+                           name="sumsq_c4", **kwargs)
+    assert float(sq(xf)) == float(np.float32(reps * float(np.sum(block * block))))
+    assert float(rd.sum_kernel(nd.float32, **kwargs)(xf)) == float(np.float32(
+        reps * float(block.sum())))
+    # elementwise at full size, checked through a reduction of its output
+    z = pool.alloc_uninitialized(nd.float32, (n,))
+    ew.ElementwiseKernel("float a, float *x, float b, float *z", "z[i] = a * x[i] + b",
+                         "axpb_c4", **kwargs)(2.0, xf, 3.0, z)
+    assert float(rd.sum_kernel(nd.float32, **kwargs)(z)) == float(np.float32(
+        reps * float(np.sum(2.0 * block + 3.0))))
