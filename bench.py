@@ -133,26 +133,38 @@ class Dist:
         if self.world != gpus and "WORLD_SIZE" in os.environ:
             print(f"warning: --gpus {gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
         self.torch = None
-        if self.world > 1:
+        # RTCG_BENCH_FORCE_DIST=1 runs the multi-GPU code path (process group,
+        # NCCL all-gather of partials) even at world size 1
+        self.forced = os.environ.get("RTCG_BENCH_FORCE_DIST") == "1"
+        if self.world > 1 or self.forced:
+            if "MASTER_ADDR" not in os.environ:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29517")
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(self.local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
             self.torch, self.dist = torch, dist
 
+    @property
+    def distributed(self) -> bool:
+        return self.torch is not None
+
     def barrier(self):
-        if self.world > 1:
+        if self.distributed:
             self.dist.barrier()
 
     def max(self, value: float) -> float:
-        if self.world == 1:
+        if not self.distributed:
             return value
         t = self.torch.tensor([value], dtype=self.torch.float64, device="cuda")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def close(self):
-        if self.world > 1:
+        if self.distributed:
             self.dist.destroy_process_group()
 
 
@@ -238,7 +250,7 @@ def run_ours(args) -> int:
 
     rt.set_device(d.local)
     info = rt.device_info(d.local)
-    stream_handle = d.torch.cuda.current_stream().cuda_stream if d.world > 1 else 0
+    stream_handle = d.torch.cuda.current_stream().cuda_stream if d.distributed else 0
     pool = nd.MemoryPool(device=d.local)
     n = N_PER_GPU
     total_n = n * d.world
@@ -267,7 +279,7 @@ def run_ours(args) -> int:
         kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
         out = pool.alloc_uninitialized(nd.float32, ())
 
-        if d.world == 1:
+        if not d.distributed:
             def step():
                 kernel.launch(gx, gy, out=out)
         else:
@@ -286,7 +298,7 @@ def run_ours(args) -> int:
         launches0 = kernel.launches
         with ClockSampler(d.local) as clocks:
             total_ms, per_step = _time_steps(rt, step, args.steps)
-        launches = kernel.launches - launches0 + (args.steps if d.world > 1 else 0)
+        launches = kernel.launches - launches0 + (args.steps if d.distributed else 0)
         rt.synchronize()
         d.barrier()
         step_ms = d.max(total_ms / args.steps)
@@ -332,7 +344,8 @@ def run_ours(args) -> int:
                    "variant": best, "autotune_seconds": round(tune_s, 2),
                    "autotune_from_store": tuned.from_store,
                    "l2": "inputs 2 GiB per GPU > 126 MB L2 (no flush needed)",
-                   "parallelism": f"shards{d.world}", "accumulator": "float64",
+                   "parallelism": f"shards{d.world}" + ("+nccl" if d.distributed else ""),
+                   "accumulator": "float64",
                    "gpu": info["name"], "result_finite": terms_ok},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
