@@ -138,8 +138,12 @@ class Dist:
         self.forced = os.environ.get("RTCG_BENCH_FORCE_DIST") == "1"
         if self.world > 1 or self.forced:
             if "MASTER_ADDR" not in os.environ:
+                import socket
+                with socket.socket() as sock:
+                    sock.bind(("127.0.0.1", 0))
+                    port = sock.getsockname()[1]
                 os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                os.environ.setdefault("MASTER_PORT", "29517")
+                os.environ.setdefault("MASTER_PORT", str(port))
                 os.environ.setdefault("RANK", "0")
                 os.environ.setdefault("WORLD_SIZE", "1")
             import torch
