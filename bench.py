@@ -224,7 +224,7 @@ def run_reference(args) -> int:
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -379,7 +379,7 @@ def run_ours(args) -> int:
         except Exception as exc:  # pragma: no cover - report, don't fail the bench
             line["cpu_baseline"] = {"value": None, "error": str(exc)}
     if d.rank == 0:
-        print(json.dumps(line))
+        emit(line)
     d.close()
     return 0
 
@@ -460,6 +460,27 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
     return out
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict) -> None:
+    """Write the one JSON result line to the real stdout (native libraries --
+    NCCL's version banner, for one -- were redirected to stderr)."""
+    text = json.dumps(line) + "\n"
+    if _JSON_OUT is None:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_OUT, text.encode())
+
+
+def _isolate_stdout() -> None:
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.dup(1)
+    os.dup2(2, 1)
+
+
 def main(argv=None) -> int:
     p = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     p.add_argument("--gpus", type=int, default=1)
@@ -469,6 +490,7 @@ def main(argv=None) -> int:
     p.add_argument("--quick", action="store_true", help="skip the secondary workloads")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     args = p.parse_args(argv)
+    _isolate_stdout()
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
