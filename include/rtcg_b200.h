@@ -52,6 +52,7 @@ typedef struct rtcg_module_s *rtcg_module_t;     /* CUmodule   */
 typedef struct rtcg_function_s *rtcg_function_t; /* CUfunction */
 typedef struct rtcg_stream_s *rtcg_stream_t;     /* CUstream; NULL = legacy default */
 typedef struct rtcg_event_s *rtcg_event_t;       /* CUevent    */
+typedef struct rtcg_graph_s *rtcg_graph_t;       /* CUgraphExec (instantiated) */
 
 typedef struct rtcg_device_info {
     char name[128];
@@ -134,6 +135,15 @@ int rtcg_event_destroy(rtcg_event_t event);
 int rtcg_event_record(rtcg_event_t event, rtcg_stream_t stream);
 int rtcg_event_synchronize(rtcg_event_t event);
 int rtcg_event_elapsed_ms(rtcg_event_t start, rtcg_event_t end, float *ms);
+
+/* --- CUDA graphs (no reference equivalent: replays a captured sequence of
+ * generated-kernel launches with one launch, for launch-bound small-n
+ * chains).  Capture must use a created stream, not the legacy default. */
+int rtcg_stream_begin_capture(rtcg_stream_t stream);
+/* Ends capture and instantiates the graph. */
+int rtcg_stream_end_capture(rtcg_stream_t stream, rtcg_graph_t *graph);
+int rtcg_graph_launch(rtcg_graph_t graph, rtcg_stream_t stream);
+int rtcg_graph_destroy(rtcg_graph_t graph);
 
 #ifdef __cplusplus
 }

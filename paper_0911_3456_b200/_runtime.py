@@ -143,6 +143,10 @@ _PROTOTYPES = {
     "rtcg_event_record": (_vp, _vp),
     "rtcg_event_synchronize": (_vp,),
     "rtcg_event_elapsed_ms": (_vp, _vp, ctypes.POINTER(ctypes.c_float)),
+    "rtcg_stream_begin_capture": (_vp,),
+    "rtcg_stream_end_capture": (_vp, ctypes.POINTER(_vp)),
+    "rtcg_graph_launch": (_vp, _vp),
+    "rtcg_graph_destroy": (_vp,),
 }
 
 EXPORTED_SYMBOLS = tuple(sorted(_PROTOTYPES)) + (
@@ -370,6 +374,27 @@ class Event:
                 _lib.rtcg_event_destroy(handle)
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
+
+
+# --- graphs ------------------------------------------------------------------------------
+
+
+def begin_capture(stream: int) -> None:
+    _check(lib().rtcg_stream_begin_capture(stream or None), "begin capture")
+
+
+def end_capture(stream: int) -> int:
+    out = _vp()
+    _check(lib().rtcg_stream_end_capture(stream or None, ctypes.byref(out)), "end capture")
+    return out.value
+
+
+def graph_launch(graph: int, stream: int) -> None:
+    _check(lib().rtcg_graph_launch(graph, stream or None), "graph launch")
+
+
+def graph_destroy(graph: int) -> None:
+    _check(lib().rtcg_graph_destroy(graph), "graph destroy")
 
 
 # --- modules and launches ------------------------------------------------------------

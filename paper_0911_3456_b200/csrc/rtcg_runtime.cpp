@@ -91,6 +91,12 @@ struct Driver {
     X(cuEventSynchronize, CUresult(CUevent))                               \
     X(cuEventElapsedTime, CUresult(float *, CUevent, CUevent))             \
     X(cuGetErrorName, CUresult(CUresult, const char **))                   \
+    X(cuStreamBeginCapture_v2, CUresult(CUstream, CUstreamCaptureMode))      \
+    X(cuStreamEndCapture, CUresult(CUstream, CUgraph *))                     \
+    X(cuGraphInstantiateWithFlags, CUresult(CUgraphExec *, CUgraph, unsigned long long)) \
+    X(cuGraphLaunch, CUresult(CUgraphExec, CUstream))                        \
+    X(cuGraphExecDestroy, CUresult(CUgraphExec))                             \
+    X(cuGraphDestroy, CUresult(CUgraph))                                     \
     X(cuGetErrorString, CUresult(CUresult, const char **))
 #define RTCG_DECLARE(name, sig) fnptr<sig> name = nullptr;
     RTCG_DRIVER_FNS(RTCG_DECLARE)
@@ -575,6 +581,43 @@ int rtcg_event_elapsed_ms(rtcg_event_t start, rtcg_event_t end, float *ms) {
     CU_CALL(g_drv.cuEventElapsedTime(ms, reinterpret_cast<CUevent>(start),
                                      reinterpret_cast<CUevent>(end)),
             "cuEventElapsedTime");
+    return RTCG_OK;
+}
+
+int rtcg_stream_begin_capture(rtcg_stream_t stream) {
+    if (!stream) return fail(RTCG_ERR_INVALID, "cannot capture the legacy default stream");
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuStreamBeginCapture_v2(reinterpret_cast<CUstream>(stream),
+                                          CU_STREAM_CAPTURE_MODE_RELAXED),
+            "cuStreamBeginCapture");
+    return RTCG_OK;
+}
+
+int rtcg_stream_end_capture(rtcg_stream_t stream, rtcg_graph_t *graph) {
+    NEED_CONTEXT();
+    CUgraph g = nullptr;
+    CU_CALL(g_drv.cuStreamEndCapture(reinterpret_cast<CUstream>(stream), &g),
+            "cuStreamEndCapture");
+    CUgraphExec exec = nullptr;
+    CUresult r = g_drv.cuGraphInstantiateWithFlags(&exec, g, 0);
+    g_drv.cuGraphDestroy(g);
+    if (r != CUDA_SUCCESS) return cu_fail(r, "cuGraphInstantiate");
+    *graph = reinterpret_cast<rtcg_graph_t>(exec);
+    return RTCG_OK;
+}
+
+int rtcg_graph_launch(rtcg_graph_t graph, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuGraphLaunch(reinterpret_cast<CUgraphExec>(graph),
+                                reinterpret_cast<CUstream>(stream)),
+            "cuGraphLaunch");
+    return RTCG_OK;
+}
+
+int rtcg_graph_destroy(rtcg_graph_t graph) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuGraphExecDestroy(reinterpret_cast<CUgraphExec>(graph)),
+            "cuGraphExecDestroy");
     return RTCG_OK;
 }
 
