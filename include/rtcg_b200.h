@@ -101,6 +101,8 @@ int rtcg_module_function(rtcg_module_t module, const char *name,
 int rtcg_function_occupancy(rtcg_function_t function, int block_threads,
                             size_t dynamic_smem, int *blocks_per_sm);
 int rtcg_function_registers(rtcg_function_t function, int *num_regs);
+/* Opt a function in to more than 48 KB of dynamic shared memory. */
+int rtcg_function_set_max_dynamic_smem(rtcg_function_t function, int bytes);
 
 /* --- launch (replaces KernelHandle.__call__, src/jit.py:553-554) --------
  * `params` follows cuLaunchKernel: params[k] points at the value of kernel

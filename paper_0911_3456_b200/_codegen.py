@@ -43,7 +43,36 @@ CACHE_POLICIES = {
     "default": (1, 0, 0),
     "streaming": (2, 2, 1),
     "no-l1": (3, 0, 2),
+    # reductions: read-only inputs staged through shared memory by TMA bulk
+    # copies (templates/reduction.cu "TMA path"); elementwise kernels treat it
+    # as "default"
+    "tma": (1, 0, 0),
 }
+TMA_STAGES = 4
+TMA_STAGE_BYTES = 32 * 1024
+TMA_HEADER = 128
+
+
+def tma_parts(sig, access, width: int) -> dict:
+    """Bindings of the reduction template's TMA path: ring buffers (one per
+    used vector), bulk copies, shared-memory chunk loads and the dynamic
+    shared-memory size."""
+    used = [p for p in sig.vectors if access[p.name].used]
+    per_elem = sum(p.dtype.size for p in used)
+    tile = max(width * 16, (TMA_STAGE_BYTES // per_elem) // width * width)
+    rings, bulks, loads = [], [], []
+    offset = 0
+    for p in used:
+        c = p.dtype.cname
+        rings.append(f"    {c} *rtcg_r_{p.name} = reinterpret_cast<{c} *>(rtcg_ring + {offset});")
+        bulks.append(f"                    rtcg::tma::bulk_load(rtcg_r_{p.name} + s * TE, "
+                     f"{p.name} + t * TE, (unsigned)(TE * sizeof({c})), rtcg_full + s);")
+        loads.append(f"                    rtcg::tma::load_smem(rtcg_v_{p.name}[u], "
+                     f"rtcg_r_{p.name} + s * TE, c);")
+        offset += TMA_STAGES * tile * p.dtype.size
+    return {"tma": True, "stages": TMA_STAGES, "tile": tile, "tile_bytes": tile * per_elem,
+            "ring_decls": "\n".join(rings), "bulk_loads": "\n".join(bulks),
+            "smem_loads": "\n".join(loads), "tma_smem": TMA_HEADER + offset}
 
 _CONTROL = re.compile(r"\b(?:if|else|for|while|do|switch|case|goto|return|break|continue)\b|[{}]")
 
@@ -151,6 +180,7 @@ def parts(sig, access, width: int, policy: str) -> dict:
             lane_args.append(f", {p.name}")
     return {
         "vector": vec_ok,
+        "tma": False,
         "width": width,
         "op_tparams": ", ".join(op_tparams),
         "op_params": "".join(op_params),
@@ -303,28 +333,28 @@ _grid_cache: dict = {}
 
 
 def grid_for(function: int, device: int, block: int, workers: int | None,
-             n: int, per_thread: int, waves: int = 1) -> int:
+             n: int, per_thread: int, waves: int = 1, smem: int = 0) -> int:
     """CTAs to launch: explicit ``workers``; else ``waves`` x the resident CTAs
     (SMs x occupancy), never more than the work needs; ``waves=0`` = exactly
     the work (one step per thread)."""
-    key = (function, device, block, workers, n, per_thread, waves)
+    key = (function, device, block, workers, n, per_thread, waves, smem)
     hit = _grid_cache.get(key)
     if hit is not None:
         return hit
     if len(_grid_cache) > 4096:
         _grid_cache.clear()
     grid = _grid_cache[key] = _compute_grid(function, device, block, workers, n, per_thread,
-                                            waves)
+                                            waves, smem)
     return grid
 
 
-def _compute_grid(function, device, block, workers, n, per_thread, waves) -> int:
+def _compute_grid(function, device, block, workers, n, per_thread, waves, smem=0) -> int:
     useful = max(1, -(-n // (block * per_thread)))
     if workers is not None:
         grid = workers
     elif waves == 0:
         grid = useful
     else:
-        resident = sm_count(device) * max(1, _runtime.occupancy(function, block))
+        resident = sm_count(device) * max(1, _runtime.occupancy(function, block, smem))
         grid = min(resident * waves, useful)
     return max(1, min(grid, 2**31 - 1))

@@ -123,6 +123,7 @@ _PROTOTYPES = {
     "rtcg_module_function": (_vp, ctypes.c_char_p, ctypes.POINTER(_vp)),
     "rtcg_function_occupancy": (_vp, _int, ctypes.c_size_t, _pint),
     "rtcg_function_registers": (_vp, _pint),
+    "rtcg_function_set_max_dynamic_smem": (_vp, _int),
     "rtcg_launch": (_vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _vp,
                     ctypes.POINTER(_vp)),
     "rtcg_mem_alloc": (_u64, ctypes.POINTER(_u64)),
@@ -425,8 +426,19 @@ class Module:
 _occupancy_cache: dict[tuple[int, int], int] = {}
 
 
+_smem_optin: dict[int, int] = {}
+
+
+def set_max_dynamic_smem(function: int, nbytes: int) -> None:
+    """Allow ``function`` to launch with ``nbytes`` of dynamic shared memory."""
+    if _smem_optin.get(function, 0) >= nbytes:
+        return
+    _check(lib().rtcg_function_set_max_dynamic_smem(function, nbytes), "smem opt-in")
+    _smem_optin[function] = nbytes
+
+
 def occupancy(function: int, block: int, smem: int = 0) -> int:
-    key = (function, block)
+    key = (function, block, smem)
     hit = _occupancy_cache.get(key)
     if hit is None:
         out = ctypes.c_int()

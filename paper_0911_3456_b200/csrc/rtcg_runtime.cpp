@@ -65,6 +65,7 @@ struct Driver {
     X(cuModuleUnload, CUresult(CUmodule))                                  \
     X(cuModuleGetFunction, CUresult(CUfunction *, CUmodule, const char *)) \
     X(cuFuncGetAttribute, CUresult(int *, CUfunction_attribute, CUfunction)) \
+    X(cuFuncSetAttribute, CUresult(CUfunction, CUfunction_attribute, int))   \
     X(cuOccupancyMaxActiveBlocksPerMultiprocessor,                             \
       CUresult(int *, CUfunction, int, size_t))                            \
     X(cuLaunchKernel, CUresult(CUfunction, unsigned, unsigned, unsigned,   \
@@ -448,6 +449,14 @@ int rtcg_function_registers(rtcg_function_t function, int *num_regs) {
     CU_CALL(g_drv.cuFuncGetAttribute(num_regs, CU_FUNC_ATTRIBUTE_NUM_REGS,
                                      reinterpret_cast<CUfunction>(function)),
             "cuFuncGetAttribute");
+    return RTCG_OK;
+}
+
+int rtcg_function_set_max_dynamic_smem(rtcg_function_t function, int bytes) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuFuncSetAttribute(reinterpret_cast<CUfunction>(function),
+                                     CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes),
+            "cuFuncSetAttribute(MAX_DYNAMIC_SHARED_SIZE_BYTES)");
     return RTCG_OK;
 }
 

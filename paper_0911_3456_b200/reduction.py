@@ -106,6 +106,9 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
         access = None  # a map expression with side effects stays general
     width = cg.chunk_width(sig, access) if access is not None else 0
     b = cg.parts(sig, access, width, variant.cache)
+    if variant.cache == "tma" and b["vector"]:
+        b.update(cg.tma_parts(sig, access, width))
+        b["vector"] = False  # the TMA entry point takes the vector path's name
     b["map_tparams"] = b.pop("op_tparams")
     b["map_params"] = b.pop("op_params")
     b.update(name=name, unroll=variant.unroll, block=variant.block, chunking=_CHUNK_TOKEN[variant.chunking],
@@ -191,6 +194,13 @@ class ReductionKernel:
         self.module = jit.compile(self.source, config, cache)
         self.generic = jit.get_kernel(self.module, f"{name}_g")
         self.vectorized = jit.get_kernel(self.module, name) if self.access and self.width else None
+        self.smem = 0
+        self._tma_tile = 0
+        if self.vectorized is not None and self.variant.cache == "tma":
+            if self.variant.block < 64:
+                raise ValueError("the TMA path needs block >= 64 (a producer warp + consumers)")
+            tp = cg.tma_parts(sig, access, self.width)
+            self.smem, self._tma_tile = tp["tma_smem"], tp["tile"]
         self.combine = jit.get_kernel(self.module, f"{name}_combine")
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
         self._binder = cg.Binder(sig, extra=4)
@@ -219,12 +229,16 @@ class ReductionKernel:
             return s
 
     def _pick(self, vectors, n):
+        """(handle, elements per thread-step, dynamic shared memory)."""
         if self.vectorized is not None:
             used = [(addr, local, p.dtype.size, self.access[p.name])
                     for p, addr, local in vectors if self.access[p.name].used]
             if cg.vector_path_ok(used, n):
-                return self.vectorized, self.variant.unroll * self.width
-        return self.generic, self.variant.unroll
+                if self.smem:
+                    return self.vectorized, max(1, self._tma_tile // self.variant.block), \
+                        self.smem
+                return self.vectorized, self.variant.unroll * self.width, 0
+        return self.generic, self.variant.unroll, 0
 
     def _read(self, address: int, dtype: Dtype):
         box = nd.ctype_for(dtype)()
@@ -271,10 +285,12 @@ class ReductionKernel:
             s.ensure(1)
             self._launch_combine(s.partials, 0, s.result, out_addr, stream)
             return s
-        handle, per_thread = self._pick(vectors, n)
+        handle, per_thread, smem = self._pick(vectors, n)
         fn = handle.function(dev)
+        if smem:
+            _runtime.set_max_dynamic_smem(fn, smem)
         grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
-                           self._waves)
+                           self._waves, smem)
         s.ensure(grid)
         b = self._binder
         b.set_range(vals, base, base + n)
@@ -282,17 +298,21 @@ class ReductionKernel:
         vals[b.count + 3] = s.result
         vals[b.count + 4] = out_addr
         vals[b.count + 5] = s.ticket
-        _runtime.launch(fn, grid, self.variant.block, ptrs, 0, stream)
+        _runtime.launch(fn, grid, self.variant.block, ptrs, smem, stream)
         self.launches += 1
         return s
 
     def launch_config(self, *args, n: int | None = None) -> dict:
         _, vectors, n = _marshal(self.spec.signature, args, n, self.name)
-        handle, per_thread = self._pick(vectors, n)
+        handle, per_thread, smem = self._pick(vectors, n)
         dev = _runtime.current_device()
-        grid = cg.grid_for(handle.function(dev), dev, self.variant.block,
-                           self.variant.workers, max(n, 1), per_thread, self._waves)
-        return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n}
+        fn = handle.function(dev)
+        if smem:
+            _runtime.set_max_dynamic_smem(fn, smem)
+        grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, max(n, 1),
+                           per_thread, self._waves, smem)
+        return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n,
+                "smem": smem}
 
     def __call__(self, *args, n: int | None = None, stream=None,
                  return_device: bool | None = None, base: int = 0):

@@ -35,6 +35,85 @@ ${unpack}
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
                  [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
 }
+{% if tma %}
+// TMA path: a producer warp streams ${stages} ring stages of ${tile}-element
+// tiles of every input into shared memory with 1-D bulk copies (cp.async.bulk,
+// completion counted in bytes on a "full" mbarrier); the consumer warps fold
+// from shared memory and hand stages back through an "empty" mbarrier.  Tiles
+// b, b+G, b+2G... belong to CTA b; elements outside whole tiles take the
+// pointer path.
+extern "C" __global__ void __launch_bounds__(${block})
+${name}(${kparams_vector}, const long start, const long end,
+    ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
+    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket)
+{
+${unpack}
+    constexpr int E = ${width};
+    constexpr int U = 1;
+    constexpr int S = ${stages};
+    constexpr long TE = ${tile};
+    extern __shared__ __align__(128) unsigned char rtcg_smem[];
+    unsigned long long *rtcg_full = reinterpret_cast<unsigned long long *>(rtcg_smem);
+    unsigned long long *rtcg_empty = rtcg_full + S;
+    unsigned char *rtcg_ring = rtcg_smem + 128;
+${ring_decls}
+    const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+    const int consumers = (int)(blockDim.x >> 5) - 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            rtcg::tma::mbar_init(rtcg_full + s, 1);
+            rtcg::tma::mbar_init(rtcg_empty + s, (unsigned)consumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    ${acc_t} acc = ${neutral};
+    auto elem = [&](const long i) {
+        acc = rtcg_fold(acc, rtcg_map<${ptr_types_vector}>(i${call_args}));
+    };
+    const long t_lo = (start + TE - 1) / TE, t_hi = end / TE;
+    const long G = gridDim.x, b = blockIdx.x;
+    const long gtid = b * (long)blockDim.x + threadIdx.x, gstep = G * (long)blockDim.x;
+    if (t_lo >= t_hi) {
+        rtcg::for_each<1>(start + gtid, end, gstep, elem);
+    } else {
+        rtcg::for_each<1>(start + gtid, t_lo * TE, gstep, elem);
+        rtcg::for_each<1>(t_hi * TE + gtid, end, gstep, elem);
+        const long mine = b < t_hi - t_lo ? (t_hi - t_lo - b + G - 1) / G : 0;
+        if (warp == 0) {
+            if (lane_id == 0) {
+                for (long j = 0; j < mine; ++j) {
+                    const int s = (int)(j % S);
+                    if (j >= S) rtcg::tma::mbar_wait(rtcg_empty + s, (unsigned)(((j / S) - 1) & 1));
+                    const long t = t_lo + b + j * G;
+                    rtcg::tma::mbar_expect_tx(rtcg_full + s, ${tile_bytes}u);
+${bulk_loads}
+                }
+            }
+        } else {
+            const long ct = threadIdx.x - 32, cn = (long)consumers * 32;
+            for (long j = 0; j < mine; ++j) {
+                const int s = (int)(j % S);
+                rtcg::tma::mbar_wait(rtcg_full + s, (unsigned)((j / S) & 1));
+                const long t = t_lo + b + j * G;
+                for (long c = ct; c < TE / E; c += cn) {
+                    const long cu = c;
+                    constexpr int u = 0;
+${vec_decls}
+${smem_loads}
+#pragma unroll
+                    for (int k = 0; k < E; ++k)
+                        acc = rtcg_fold(acc, rtcg_map<${lane_types}>(t * TE + cu * E + k${lane_args}));
+                }
+                __syncwarp();
+                if (lane_id == 0) rtcg::tma::mbar_arrive(rtcg_empty + s);
+            }
+        }
+    }
+    rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+}
+{% endif %}
 {% if vector %}
 // Vector path: ${unroll} x 16-byte chunks per vector per thread per step,
 // loaded before the fold chain consumes them.

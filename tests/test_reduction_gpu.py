@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
 
 _VARIANTS = (ew.VariantParams(), ew.VariantParams(unroll=1, block=64, workers=7),
              ew.VariantParams(unroll=8, block=512, chunking="contiguous-blocks"),
-             ew.VariantParams(unroll=2, block=1024, workers=1))
+             ew.VariantParams(unroll=2, block=1024, workers=1),
+             ew.VariantParams(cache="tma", block=256),
+             ew.VariantParams(cache="tma", block=64, workers=3))
 
 
 def test_reference_known_answers(kernel_env, golden):
