@@ -275,7 +275,9 @@ def run_ours(args) -> int:
         # autotune block x unroll for (dot, float32, n) -- outside the timed region
         spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
         t0 = time.perf_counter()
-        tuned = at.tune_reduction(spec, "dot_k", n, at.DEFAULT_AXES, args=[gx, gy],
+        axes = dict(at.DEFAULT_AXES, cache=("default", "tma"))
+        tuned = at.tune_reduction(spec, "dot_k", n, axes, args=[gx, gy],
+                                  constraints=(lambda a: a["cache"] != "tma" or a["unroll"] == 1,),
                                   protocol=at.MeasurementProtocol(warmup=2, repeats=5),
                                   store=at.TuneStore())
         tune_s = time.perf_counter() - t0
