@@ -11,11 +11,12 @@ plumbing):
   local slice with ``base`` = the slice start, so ``i`` in user code stays the
   global index;
 * elementwise kernels need no communication;
-* reductions do one exchange: each rank's accumulator (8 bytes) is
-  all-gathered over NCCL (NVLink / NVSwitch) into a world-sized buffer and
-  every rank folds it in ascending rank order with the kernel's compiled
-  ``<name>_combine`` entry point.  This works for any ``reduce_expr`` (NCCL's
-  built-in sum/min/max would not) and is deterministic for a fixed world size.
+* reductions do one exchange over NCCL (NVLink / NVSwitch): an ncclAllReduce
+  of the 8-byte accumulators when the reduce_expr is exactly an NCCL op
+  (integer sum; max/min), otherwise an all-gather of the accumulators into a
+  world-sized buffer folded in ascending rank order by the kernel's compiled
+  ``<name>_combine`` -- valid for any ``reduce_expr`` and deterministic for a
+  fixed world size (float sums always take this path).
 """
 
 from __future__ import annotations
@@ -28,7 +29,7 @@ from . import _runtime
 from . import ndarray as nd
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
-           "sharded_reduce", "gather_partials", "ordered_fold"]
+           "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -117,28 +118,73 @@ class _DeviceView:
                                          "strides": None}
 
 
-def sharded_reduce(kernel, *args, group=None, return_device: bool = False):
+_NCCL_OPS = {"a+b": "sum", "b+a": "sum", "a>b?a:b": "max", "b>a?b:a": "max",
+             "a<b?a:b": "min", "b<a?b:a": "min"}
+
+
+def nccl_op(spec) -> str | None:
+    """The NCCL reduction equal to ``spec.reduce_expr`` *exactly*, or None.
+
+    sum is exact (order-independent) only for integer accumulators (two's
+    complement wrap); max/min are exact for every dtype on NaN-free data.
+    Float sums keep the ordered fold so results do not depend on NCCL's
+    reduction order."""
+    op = _NCCL_OPS.get("".join(spec.reduce_expr.split()))
+    if spec.acc_dtype.name not in _NCCL_DTYPES:
+        return None
+    if op == "sum" and spec.acc_dtype.kind == "f":
+        return None
+    return op
+
+
+# accumulator dtypes both NCCL and torch's NCCL backend reduce natively
+_NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
+
+
+def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
+                   collective: str = "auto"):
     """Global reduction of a ReductionKernel over sharded arguments.
 
     1. local two-stage reduction into the kernel's scratch accumulator;
-    2. NCCL all-gather of the per-rank accumulators (world x 8 bytes);
-    3. ``<name>_combine`` folds them in rank order on the device.
-    All three run in stream order on torch's current stream.
+    2. the cross-GPU step over NCCL (NVLink / NVSwitch):
+       ``"allreduce"`` -- one ncclAllReduce of the 8-byte accumulators when
+       :func:`nccl_op` maps ``reduce_expr`` to an exact NCCL op;
+       ``"allgather"`` -- all-gather (world x 8 bytes) + ``<name>_combine``
+       folding in rank order, valid for any ``reduce_expr``;
+       ``"auto"`` -- allreduce when exact, else allgather;
+    3. the out-dtype value is written on the device.
+    Everything runs in stream order on torch's current stream.
     """
     import torch
+    import torch.distributed as dist
 
     local_args, base = _locals(args)
     n_local = next(a.size for a in local_args if isinstance(a, nd.NdArray))
     spec = kernel.spec
+    op = nccl_op(spec)
+    if collective == "auto":
+        collective = "allreduce" if op is not None else "allgather"
+    if collective == "allreduce" and op is None:
+        raise ValueError(f"reduce_expr {spec.reduce_expr!r} has no exact NCCL equivalent")
+    if collective not in ("allreduce", "allgather"):
+        raise ValueError(f"unknown collective {collective!r}")
     stream = torch.cuda.current_stream().cuda_stream
     with _runtime.use_stream(stream):
         scratch = kernel.launch(*local_args, n=n_local, base=base)
         acc_view = torch.as_tensor(_DeviceView(scratch.result, 1, spec.acc_dtype), device="cuda")
-        gathered = gather_partials(acc_view, group)
-        world = gathered.numel()
         first = next(a for a in local_args if isinstance(a, nd.NdArray))
         out = first.pool.alloc_uninitialized(spec.out_dtype, ())
-        kernel._launch_combine(gathered.data_ptr(), world, scratch.result, out.address)
+        if collective == "allreduce":
+            reduce_op = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX,
+                         "min": dist.ReduceOp.MIN}[op]
+            dist.all_reduce(acc_view, op=reduce_op, group=group)
+            # fold the single global accumulator once more to write the out
+            # dtype (a fold of one value from the neutral is the identity)
+            kernel._launch_combine(scratch.result, 1, scratch.result, out.address)
+        else:
+            gathered = gather_partials(acc_view, group)
+            kernel._launch_combine(gathered.data_ptr(), gathered.numel(), scratch.result,
+                                   out.address)
         if return_device:
             # `gathered` goes back to torch's caching allocator; its reuse is
             # ordered after the combine because both run on this stream

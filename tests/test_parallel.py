@@ -30,6 +30,18 @@ def test_shard_ranges_partition(n, world):
         par.shard_range(n, world, world)
 
 
+def test_nccl_op_only_when_exact():
+    from paper_0911_3456_b200 import ndarray as nd, reduction as rd
+    spec = lambda t, red: rd.ReductionSpec(f"{t.cname} *x", t, "0", red)  # noqa: E731
+    assert par.nccl_op(spec(nd.int64, "a + b")) == "sum"
+    assert par.nccl_op(spec(nd.int32, " b+a ")) == "sum"
+    assert par.nccl_op(spec(nd.float32, "a + b")) is None        # float sum: ordered fold
+    assert par.nccl_op(spec(nd.float64, "a > b ? a : b")) == "max"
+    assert par.nccl_op(spec(nd.int8, "a < b ? a : b")) == "min"
+    assert par.nccl_op(spec(nd.int16, "a + b")) is None           # no ncclInt16
+    assert par.nccl_op(spec(nd.int64, "a * b")) is None
+
+
 def test_ordered_fold_is_left_fold():
     assert par.ordered_fold(lambda a, b: a * 10 + b, 0, [1, 2, 3]) == 123
 
@@ -110,6 +122,16 @@ def test_sharded_reduce_and_elementwise_single_rank(nccl_world1, pool):
     assert int(got) == int(cport.Reduction("int64_t *x", "int64", "0", "a + b")(host))
     dev = par.sharded_reduce(rd.sum_kernel(nd.int64), sx, return_device=True)
     assert int(dev.get()) == int(got)
+    for collective in ("allreduce", "allgather"):
+        assert int(par.sharded_reduce(rd.sum_kernel(nd.int64), sx, collective=collective)) == \
+            int(got)
+    mx = par.sharded_reduce(rd.max_kernel(nd.int64), sx, collective="allreduce")
+    assert int(mx) == int(host.max())
+    fx = par.scatter_from_host(host.astype(np.float32) * 1e-18, nd.float32, n, 0, 1, pool)
+    with pytest.raises(ValueError):
+        par.sharded_reduce(rd.sum_kernel(nd.float32), fx, collective="allreduce")
+    assert float(par.sharded_reduce(rd.sum_kernel(nd.float32), fx)) == \
+        float(rd.sum_kernel(nd.float32)(fx.local))
     out = par.ShardedArray(pool.alloc(nd.int64, (n,)), sx.base, n, 0, 1)
     par.sharded_elementwise(ew.ElementwiseKernel("long *x, long *z", "z[i] = x[i] ^ i", "xi"),
                             sx, out)
