@@ -114,6 +114,11 @@ int rtcg_launch(rtcg_function_t function, unsigned grid, unsigned block,
 /* --- device memory (replaces src/ndarray.py:158-160, :216, :316-336) ----- */
 int rtcg_mem_alloc(uint64_t nbytes, uint64_t *dptr);
 int rtcg_mem_free(uint64_t dptr);
+/* Stream-ordered allocation from the device's default memory pool (release
+ * threshold raised so freed memory stays cached by the driver): allocation
+ * and free are ordered with kernels on `stream` and never synchronise. */
+int rtcg_mem_alloc_async(uint64_t nbytes, rtcg_stream_t stream, uint64_t *dptr);
+int rtcg_mem_free_async(uint64_t dptr, rtcg_stream_t stream);
 int rtcg_memset_async(uint64_t dptr, unsigned char value, uint64_t nbytes,
                       rtcg_stream_t stream);
 int rtcg_memcpy_htod_async(uint64_t dst, const void *src, uint64_t nbytes,

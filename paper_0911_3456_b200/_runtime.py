@@ -128,6 +128,8 @@ _PROTOTYPES = {
                     ctypes.POINTER(_vp)),
     "rtcg_mem_alloc": (_u64, ctypes.POINTER(_u64)),
     "rtcg_mem_free": (_u64,),
+    "rtcg_mem_alloc_async": (_u64, _vp, ctypes.POINTER(_u64)),
+    "rtcg_mem_free_async": (_u64, _vp),
     "rtcg_memset_async": (_u64, ctypes.c_ubyte, _u64, _vp),
     "rtcg_memcpy_htod_async": (_u64, _vp, _u64, _vp),
     "rtcg_memcpy_dtoh_async": (_vp, _u64, _u64, _vp),
@@ -475,6 +477,21 @@ def mem_alloc(nbytes: int) -> int:
 
 def mem_free(dptr: int) -> None:
     _check(lib().rtcg_mem_free(dptr), "cuMemFree")
+
+
+def mem_alloc_async(nbytes: int, stream=None) -> int:
+    """Stream-ordered allocation (cuMemAllocAsync from the device mempool)."""
+    current_device()
+    s = current_stream() if stream is None else stream
+    out = _u64()
+    _check(lib().rtcg_mem_alloc_async(nbytes, s or None, ctypes.byref(out)),
+           f"cuMemAllocAsync({nbytes})")
+    return out.value
+
+
+def mem_free_async(dptr: int, stream=None) -> None:
+    s = current_stream() if stream is None else stream
+    _check(lib().rtcg_mem_free_async(dptr, s or None), "cuMemFreeAsync")
 
 
 def memset_async(dptr: int, value: int, nbytes: int, stream=None) -> None:

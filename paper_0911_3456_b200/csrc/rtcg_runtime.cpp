@@ -73,6 +73,10 @@ struct Driver {
                                    CUstream, void **, void **))                \
     X(cuMemAlloc_v2, CUresult(CUdeviceptr *, size_t))                      \
     X(cuMemFree_v2, CUresult(CUdeviceptr))                                 \
+    X(cuMemAllocAsync, CUresult(CUdeviceptr *, size_t, CUstream))            \
+    X(cuMemFreeAsync, CUresult(CUdeviceptr, CUstream))                       \
+    X(cuDeviceGetDefaultMemPool, CUresult(CUmemoryPool *, CUdevice))         \
+    X(cuMemPoolSetAttribute, CUresult(CUmemoryPool, CUmemPool_attribute, void *)) \
     X(cuMemsetD8Async, CUresult(CUdeviceptr, unsigned char, size_t, CUstream)) \
     X(cuMemcpyHtoDAsync_v2,                                                    \
       CUresult(CUdeviceptr, const void *, size_t, CUstream))               \
@@ -482,6 +486,37 @@ int rtcg_mem_alloc(uint64_t nbytes, uint64_t *dptr) {
 int rtcg_mem_free(uint64_t dptr) {
     NEED_CONTEXT();
     CU_CALL(g_drv.cuMemFree_v2(dptr), "cuMemFree");
+    return RTCG_OK;
+}
+
+static std::vector<char> g_pool_ready;  // per device: release threshold raised
+
+int rtcg_mem_alloc_async(uint64_t nbytes, rtcg_stream_t stream, uint64_t *dptr) {
+    NEED_CONTEXT();
+    {
+        std::lock_guard<std::mutex> lock(g_drv_mutex);
+        if (g_pool_ready.size() < g_primary.size()) g_pool_ready.assign(g_primary.size(), 0);
+        if (!g_pool_ready[t_device]) {
+            CUmemoryPool pool;
+            CUdevice dev;
+            CU_CALL(g_drv.cuDeviceGet(&dev, t_device), "cuDeviceGet");
+            CU_CALL(g_drv.cuDeviceGetDefaultMemPool(&pool, dev), "cuDeviceGetDefaultMemPool");
+            cuuint64_t keep = ~0ull;
+            CU_CALL(g_drv.cuMemPoolSetAttribute(pool, CU_MEMPOOL_ATTR_RELEASE_THRESHOLD, &keep),
+                    "cuMemPoolSetAttribute(RELEASE_THRESHOLD)");
+            g_pool_ready[t_device] = 1;
+        }
+    }
+    CUdeviceptr p = 0;
+    CU_CALL(g_drv.cuMemAllocAsync(&p, nbytes, reinterpret_cast<CUstream>(stream)),
+            "cuMemAllocAsync");
+    *dptr = p;
+    return RTCG_OK;
+}
+
+int rtcg_mem_free_async(uint64_t dptr, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuMemFreeAsync(dptr, reinterpret_cast<CUstream>(stream)), "cuMemFreeAsync");
     return RTCG_OK;
 }
 
