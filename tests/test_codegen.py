@@ -71,7 +71,7 @@ def test_parse_round_trips_generated_signatures(params):
 def test_variant_validation_and_defaults():
     v = ew.VariantParams()
     assert (v.unroll, v.workers, v.chunking, v.block, v.cache, v.waves) == \
-        (4, None, "strided", 256, "default", None)
+        (1, None, "strided", 256, "default", None)
     assert v.resolved() is v
     for bad in (dict(unroll=3), dict(workers=0), dict(workers=ew.MAX_WORKERS + 1),
                 dict(chunking="round-robin"), dict(block=100), dict(cache="bogus"),
