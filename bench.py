@@ -429,17 +429,38 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
                             protocol=proto, store=store)
     axpy = ew.ElementwiseKernel(sig, op, "axpy", ew.VariantParams(**t.best_assignment))
     record("axpy_f32_2p28", lambda: axpy(2.0, x, -3.0, y, z), 12 * n, t)
+    for a in (x, y, z):
+        a.free()
+
+    # C4: max|x|, L2 (sum of squares; sqrt on the host) and the wrapping int64
+    # sum at n = 2^32, inputs synthesised on the device from a hash of i
+    big = 1 << 32
+    xf = pool.alloc_uninitialized(nd.float32, (big,))
+    ew.ElementwiseKernel("float *x", "unsigned long h = (unsigned long) i * 0x9E3779B97F4A7C15UL; "
+                         "x[i] = (float) ((long) (h >> 40) - (1L << 23)) * 1.1920929e-7f",
+                         "synth_f32")(xf)
     o32 = pool.alloc_uninitialized(nd.float32, ())
     for name, mp, red in (("maxabs", "fabsf(x[i])", "a > b ? a : b"),
                           ("sumsq", "x[i] * x[i]", "a + b")):
         spec = rd.ReductionSpec("float *x", nd.float32, "0", red, mp)
-        t = at.tune_reduction(spec, name, n, at.DEFAULT_AXES, args=[x], protocol=proto,
+        t = at.tune_reduction(spec, name, big, at.DEFAULT_AXES, args=[xf], protocol=proto,
                               store=store)
         k = rd.ReductionKernel(spec, name, ew.VariantParams(**t.best_assignment))
-        record(f"{name}_f32_2p28", lambda: k.launch(x, out=o32), 4 * n, t,
-               note="L2 norm = sqrt of sumsq (host)" if name == "sumsq" else "max|x|")
-    for a in (x, y, z):
-        a.free()
+        record(f"{name}_f32_2p32", lambda: k.launch(xf, out=o32), 4 * big, t,
+               note="L2 norm = sqrt(sumsq) on the host" if name == "sumsq" else "max|x|")
+    xf.free()
+    xi = pool.alloc_uninitialized(nd.int64, (big,))
+    ew.ElementwiseKernel("long *x", "x[i] = (long) ((unsigned long) i * 0x9E3779B97F4A7C15UL) >> 1",
+                         "synth_i64")(xi)
+    o64 = pool.alloc_uninitialized(nd.int64, ())
+    spec = rd.ReductionSpec("int64_t *x", nd.int64, "0", "a + b")
+    t = at.tune_reduction(spec, "sum_k", big, at.DEFAULT_AXES, args=[xi], protocol=proto,
+                          store=store)
+    si = rd.ReductionKernel(spec, "sum_k", ew.VariantParams(**t.best_assignment))
+    record("sum_i64_2p32", lambda: si.launch(xi, out=o64), 8 * big, t,
+           note="values in [-2^62, 2^62): the sum wraps (bit-exact, order independent)")
+    xi.free()
+
     xd = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
     zd = pool.alloc_uninitialized(nd.float64, (n,))
     sig, op = ("double a, double *x, double *z",
@@ -451,14 +472,6 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
            bound="fp64 issue (double sin: ~37 DP instructions/element), not HBM")
     xd.free()
     zd.free()
-    xi = nd.from_host(pool, nd.int64, rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64))
-    o64 = pool.alloc_uninitialized(nd.int64, ())
-    spec = rd.ReductionSpec("int64_t *x", nd.int64, "0", "a + b")
-    t = at.tune_reduction(spec, "sum_k", n, at.DEFAULT_AXES, args=[xi], protocol=proto,
-                          store=store)
-    si = rd.ReductionKernel(spec, "sum_k", ew.VariantParams(**t.best_assignment))
-    record("sum_i64_2p28", lambda: si.launch(xi, out=o64), 8 * n, t)
-    xi.free()
     return out
 
 
