@@ -40,7 +40,7 @@ from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
 from .elementwise import (_CHUNK_TOKEN, _ERRORS, KernelSignature, ParseError, VariantParams,
-                          _check_name, _marshal, parse_signature)
+                          _check_name, _marshal, _preamble_text, parse_signature)
 from .ndarray import Dtype
 
 __all__ = [
@@ -96,7 +96,7 @@ class ReductionSpec:
 
 
 def generate_reduction_source(spec: ReductionSpec, name: str,
-                              variant: VariantParams) -> str:
+                              variant: VariantParams, preamble: str = "") -> str:
     """CUDA source with ``<name>`` (vector path, when legal), ``<name>_g``
     (general) and ``<name>_combine`` (ordered fold of partials)."""
     _check_name(name)
@@ -111,7 +111,8 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
         b["vector"] = False  # the TMA entry point takes the vector path's name
     b["map_tparams"] = b.pop("op_tparams")
     b["map_params"] = b.pop("op_params")
-    b.update(name=name, unroll=variant.unroll, block=variant.block, chunking=_CHUNK_TOKEN[variant.chunking],
+    b.update(name=name, unroll=variant.unroll, block=variant.block,
+             preamble=_preamble_text(preamble), chunking=_CHUNK_TOKEN[variant.chunking],
              acc_t=spec.acc_dtype.cname, out_t=spec.out_dtype.cname,
              neutral=spec.neutral, reduce_expr=spec.reduce_expr, map_expr=spec.mapped)
     return cg.render("reduction.cu", b)
@@ -168,23 +169,27 @@ class ReductionKernel:
 
     def _init_pycuda(self, dtype_out=None, neutral=None, reduce_expr=None, map_expr=None,
                      arguments=None, name="reduce_kernel", variant=None, *,
-                     config=None, cache=None, debug=False, return_device=True, **_ignored):
+                     config=None, cache=None, debug=False, return_device=True, preamble="",
+                     **_ignored):
         if arguments is None:
             raise ParseError("ReductionKernel needs an 'arguments' signature")
         spec = ReductionSpec(arguments, nd.dtype_of(dtype_out), str(neutral), reduce_expr,
                              map_expr)
-        self._init_reference(spec, name, variant, config=config, cache=cache, debug=debug)
+        self._init_reference(spec, name, variant, config=config, cache=cache, debug=debug,
+                             preamble=preamble)
         self.return_device = return_device
 
     def _init_reference(self, spec: ReductionSpec, name: str = "reduce",
                         variant: VariantParams | None = None, *,
                         config: jit.ToolchainConfig | None = None,
-                        cache: jit.CacheStore | None = None, debug: bool = False) -> None:
+                        cache: jit.CacheStore | None = None, debug: bool = False,
+                        preamble: str = "") -> None:
         self.spec = spec
+        self.preamble = preamble
         self.name = name
         self.variant = (variant or VariantParams()).resolved()
         self.return_device = False
-        self.source = generate_reduction_source(spec, name, self.variant)
+        self.source = generate_reduction_source(spec, name, self.variant, preamble)
         sig = spec.signature
         access = cg.analyze(spec.mapped, [p.name for p in sig.vectors])
         if access is not None and any(a.written for a in access.values()):

@@ -1,4 +1,5 @@
 ${prelude}
+${preamble}
 // ---- elementwise kernel "${name}" (templates/elementwise.cu) ---------------
 // The user's statement, verbatim, as the body of one per-element function.
 // It is instantiated twice: with real pointers (general path) and with

@@ -1,4 +1,5 @@
 ${prelude}
+${preamble}
 // ---- reduction kernel "${name}" (templates/reduction.cu) --------------------
 // reduce_expr over a and b, and map_expr over the parameters and i, verbatim.
 // rtcg_fold(acc, map) is the reference's textual "acc = reduce(a->acc,

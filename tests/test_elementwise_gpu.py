@@ -403,3 +403,24 @@ def test_pinned_host_round_trip(pool):
     out = nd.pinned_empty((n,), nd.float32)
     g.to_host(out=out)
     assert np.array_equal(out, h)
+
+
+def test_preamble_and_range(kernel_env):
+    kwargs, pool = kernel_env
+    pre = "__device__ float cube(float v) { return v * v * v; }"
+    k = ew.ElementwiseKernel("float *x, float *z", "z[i] = cube(x[i])", "cubed",
+                             preamble=pre, **kwargs)
+    assert "__device__ float cube" in k.source and k.vectorized is not None
+    h = np.arange(1000, dtype=np.float32) - 500
+    x = nd.from_host(pool, nd.float32, h)
+    z = nd.from_host(pool, nd.float32, np.full(1000, -1.0, np.float32))
+    k(x, z, range=slice(10, 990))
+    want = np.full(1000, -1.0, np.float32)
+    want[10:990] = h[10:990] * h[10:990] * h[10:990]
+    assert np.array_equal(z.get(), want)
+    with pytest.raises(ValueError):
+        k(x, z, range=slice(0, 10, 2))
+    from paper_0911_3456_b200 import reduction as rd
+    r = rd.ReductionKernel(np.float32, "0", "a + b", "cube(x[i])", "float *x", preamble=pre,
+                           cache=kwargs["cache"], config=kwargs["config"])
+    assert float(r(x).get()) == float(np.float32(np.sum((h.astype(np.float64)) ** 3)))
