@@ -423,4 +423,5 @@ def test_preamble_and_range(kernel_env):
     from paper_0911_3456_b200 import reduction as rd
     r = rd.ReductionKernel(np.float32, "0", "a + b", "cube(x[i])", "float *x", preamble=pre,
                            cache=kwargs["cache"], config=kwargs["config"])
-    assert float(r(x).get()) == float(np.float32(np.sum((h.astype(np.float64)) ** 3)))
+    cubes = (h * h * h).astype(np.float64)      # float products, exact fp64 sum
+    assert float(r(x).get()) == float(np.float32(np.sum(cubes)))
