@@ -158,3 +158,71 @@ def test_shard_slices_keep_global_index(pool):
     per_rank = [mx.launch(par.scatter_from_host(host, nd.float64, n, r, 3, pool).local) and
                 mx._read(mx.scratch(0).out, nd.float64) for r in range(3)]
     assert max(per_rank) == host.max()
+
+
+def _gpu_rank(rank, world, port, cache_dir, queue):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RTCG_CACHE_DIR=cache_dir)
+    from paper_0911_3456_b200 import _runtime, elementwise as ew, ndarray as nd, reduction as rd
+    _runtime.set_device(0)
+    import torch
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = 3_000_017
+        rng = np.random.default_rng(77)
+        hi = rng.integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
+        hf = rng.uniform(-1, 1, n).astype(np.float32)
+        pool = nd.MemoryPool(device=0)
+        si = par.scatter_from_host(hi, nd.int64, n, rank, world, pool)
+        sf = par.scatter_from_host(hf, nd.float32, n, rank, world, pool)
+        out = {
+            "sum_i64_allreduce": int(par.sharded_reduce(rd.sum_kernel(nd.int64), si,
+                                                        collective="allreduce")),
+            "sum_i64_allgather": int(par.sharded_reduce(rd.sum_kernel(nd.int64), si,
+                                                        collective="allgather")),
+            "max_f32": float(par.sharded_reduce(rd.max_kernel(nd.float32), sf)),
+            "sum_f32": float(par.sharded_reduce(rd.sum_kernel(nd.float32), sf)),
+        }
+        z = par.ShardedArray(pool.alloc(nd.int64, (si.local.size,)), si.base, n, rank, world)
+        par.sharded_elementwise(ew.ElementwiseKernel("long *x, long *z", "z[i] = x[i] + i", "xpi"),
+                                si, z)
+        lo, hi_ = par.shard_range(n, rank, world)
+        out["elementwise_ok"] = bool(np.array_equal(z.local.get(),
+                                                     hi[lo:hi_] + np.arange(lo, hi_)))
+        queue.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_ranks_sharing_the_gpu_reduce_like_one(tmp_path):
+    """World size 2 (gloo; both ranks on the one B200): the sharded reductions
+    and elementwise kernels equal the single-process results."""
+    import multiprocessing as mp
+    from oracle import csem, cport
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_rank, args=(r, 2, port, str(tmp_path / "c"), q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    n = 3_000_017
+    rng = np.random.default_rng(77)
+    hi = rng.integers(-(1 << 62), 1 << 62, size=n, dtype=np.int64)
+    hf = rng.uniform(-1, 1, n).astype(np.float32)
+    want_i = int(cport.Reduction("int64_t *x", "int64", "0", "a + b")(hi))
+    for r in (0, 1):
+        got = results[r]
+        assert got["sum_i64_allreduce"] == want_i == got["sum_i64_allgather"]
+        assert got["max_f32"] == float(hf.max())
+        terms = hf.astype(np.float64)
+        assert abs(got["sum_f32"] - csem.exact_sum(terms)) <= \
+            csem.float_reduction_bound(terms, "float32")
+        assert got["elementwise_ok"]
+    assert results[0] == results[1]           # every rank holds the same answer
