@@ -262,15 +262,15 @@ def test_auto_kernels_tune_once_per_bucket(pool, tmp_path, shared_cache):
     axes = {"unroll": (1, 4), "block": (128, 256)}
     k = at.AutoElementwise("float *x, float *z", "z[i] += x[i]", "acc_add", axes, store=store,
                            cache=shared_cache, pool=pool)
-    x = nd.from_host(pool, nd.float32, np.ones(5000, np.float32))
-    z = nd.from_host(pool, nd.float32, np.full(5000, 2.0, np.float32))
-    k(x, z)                          # tuning happens on synthetic data, not on z
-    assert np.all(z.get() == 3.0)    # the in-place statement ran exactly once
-    k(x, z, n=4000)                  # same bucket: no new campaign
+    x = nd.from_host(pool, nd.float32, np.ones(8000, np.float32))
+    z = nd.from_host(pool, nd.float32, np.full(8000, 2.0, np.float32))
+    k(x, z, n=5000)                  # tuning happens on synthetic data, not on z
+    assert np.all(z.get()[:5000] == 3.0) and np.all(z.get()[5000:] == 2.0)
+    k(x, z, n=8000)                  # same bucket (8192): no new campaign
     assert len(k.results) == 1 and k.results[8192].best_assignment in \
         at.ParamSpace.make(axes).enumerate()
     spec = rd.ReductionSpec("float *x", nd.float32, "0", "a + b")
     r = at.AutoReduction(spec, "auto_sum", axes, store=store, cache=shared_cache, pool=pool)
-    assert float(r(x)) == 5000.0 and len(r.results) == 1
+    assert float(r(x)) == 8000.0 and len(r.results) == 1
     again = at.AutoReduction(spec, "auto_sum", axes, store=store, cache=shared_cache, pool=pool)
-    assert float(again(x)) == 5000.0 and again.results[8192].from_store
+    assert float(again(x)) == 8000.0 and again.results[8192].from_store
