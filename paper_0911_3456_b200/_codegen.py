@@ -243,6 +243,9 @@ class Binder:
         self.count = len(self.params)
         self.total = self.count + 2 + extra
         self._tls = threading.local()
+        # (slot, is_vector, dtype, element size, scalar kind, name) per parameter
+        self._plan = tuple((k, p.is_vector, p.dtype, p.dtype.size, p.dtype.kind, p.name, p)
+                           for k, p in enumerate(self.params))
 
     def slots(self):
         held = getattr(self._tls, "slots", None)
@@ -256,35 +259,41 @@ class Binder:
     def bind(self, args, n, base: int, name: str, errors):
         """-> (vals, ptrs, vectors, n); ``vectors`` = [(param, addr0, local)].
         ``errors`` = (ArityMismatch, DtypeMismatch, ShapeMismatch, NdArray)."""
-        arity, dtype_err, shape_err, array_t = errors
-        params = self.params
         if len(args) != self.count:
-            raise arity(f"kernel {name} takes {self.count} arguments, got {len(args)}")
-        vals, ptrs = self.slots()
+            raise errors[0](f"kernel {name} takes {self.count} arguments, got {len(args)}")
+        array_t = errors[3]
+        try:
+            vals, ptrs = self._tls.slots
+        except AttributeError:
+            vals, ptrs = self.slots()
         vectors = []
-        for k, p in enumerate(params):
+        for k, is_vector, dtype, size, kind, pname, p in self._plan:
             arg = args[k]
-            if p.is_vector:
-                if not isinstance(arg, array_t):
-                    raise dtype_err(p.name, f"expected a GPUArray, got {type(arg).__name__}")
-                if arg.dtype is not p.dtype and arg.dtype != p.dtype:
-                    raise dtype_err(p.name, f"expected dtype {p.dtype.name}, "
-                                            f"got {arg.dtype.name}")
+            if is_vector:
+                if arg.__class__ is not array_t and not isinstance(arg, array_t):
+                    raise errors[1](pname, f"expected a GPUArray, got {type(arg).__name__}")
+                if arg.dtype is not dtype and arg.dtype != dtype:
+                    raise errors[1](pname, f"expected dtype {dtype.name}, got {arg.dtype.name}")
+                asize = arg.size
                 if n is None:
-                    n = arg.size
-                if arg.size < n:
-                    raise shape_err(f"vector {p.name!r} holds {arg.size} elements, "
+                    n = asize
+                elif asize < n:
+                    raise errors[2](f"vector {pname!r} holds {asize} elements, "
                                     f"kernel span is {n}")
-                local = arg.address
-                addr0 = (local - base * p.dtype.size) & _MASK64
+                if arg._freed:
+                    raise ValueError("array was freed")
+                block = arg._block
+                local = block.address if block is not None else 0
+                addr0 = (local - base * size) & _MASK64 if base else local
                 vals[k] = addr0
                 vectors.append((p, addr0, local))
             else:
                 if isinstance(arg, array_t):
-                    raise dtype_err(p.name, "expected a scalar, got a GPUArray")
-                vals[k] = _bits(arg, p.dtype.kind)
+                    raise errors[1](pname, "expected a scalar, got a GPUArray")
+                vals[k] = _UNPACK_Q(_PACK_D(float(arg)))[0] if kind == "f" \
+                    else int(arg) & _MASK64
         if n is None:
-            raise arity("cannot infer n: no vector arguments")
+            raise errors[0]("cannot infer n: no vector arguments")
         return vals, ptrs, vectors, n
 
     def set_range(self, vals, start: int, end: int) -> None:

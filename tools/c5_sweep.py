@@ -65,7 +65,24 @@ def main():
         k(2.0, x, z)
     rt.synchronize()
     per_launch = (time.perf_counter() - t0) / 1000
+    # the same call captured in a CUDA graph: host cost per replay
+    from paper_0911_3456_b200 import graph as gr
+    g = gr.Graph()
+    with rt.use_stream(g.stream):
+        k(2.0, x, z)
+        g.synchronize()
+    with g.capture():
+        for _ in range(10):
+            k(2.0, x, z)
+    g.launch()
+    g.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(100):
+        g.launch()
+    g.synchronize()
+    per_graph_kernel = (time.perf_counter() - t0) / 1000
     report["latency"] = {"cold_nvrtc_construct_ms": round(cold * 1e3, 2),
+                         "graph_replay_us_per_kernel": round(per_graph_kernel * 1e6, 2),
                          "warm_cache_construct_ms_median": round(sorted(warm)[10] * 1e3, 3),
                          "cold_over_warm": round(cold / sorted(warm)[10], 1),
                          "host_call_us_back_to_back": round(per_launch * 1e6, 2)}
