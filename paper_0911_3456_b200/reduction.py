@@ -40,7 +40,7 @@ from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
 from .elementwise import (_CHUNK_TOKEN, _ERRORS, KernelSignature, ParseError, VariantParams,
-                          _check_name, _marshal, _preamble_text, parse_signature)
+                          _check_name, _preamble_text, parse_signature)
 from .ndarray import Dtype
 
 __all__ = [
@@ -308,7 +308,7 @@ class ReductionKernel:
         return s
 
     def launch_config(self, *args, n: int | None = None) -> dict:
-        _, vectors, n = _marshal(self.spec.signature, args, n, self.name)
+        _, _, vectors, n = self._binder.bind(args, n, 0, self.name, _ERRORS)
         handle, per_thread, smem = self._pick(vectors, n)
         dev = _runtime.current_device()
         fn = handle.function(dev)
