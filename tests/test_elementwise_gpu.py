@@ -425,3 +425,38 @@ def test_preamble_and_range(kernel_env):
                            cache=kwargs["cache"], config=kwargs["config"])
     cubes = (h * h * h).astype(np.float64)      # float products, exact fp64 sum
     assert float(r(x).get()) == float(np.float32(np.sum(cubes)))
+
+
+@pytest.mark.parametrize("n", [1, 3, 17, 1000, 65_537, 1_000_003])
+def test_partition_covers_every_index_exactly_once(kernel_env, n):
+    """SPEC 'worker-range partition' invariant, GPU form: a guard array
+    incremented once per visited index ends up all ones inside [0, n) and
+    untouched outside, for every partition / grid policy and both paths."""
+    kwargs, pool = kernel_env
+    guard = pool.alloc(nd.int32, (n + 5,))
+    variants = [ew.VariantParams(unroll=u, block=b, chunking=c, waves=w, workers=wk)
+                for u, b, c, w, wk in ((1, 256, "strided", None, None), (4, 64, "strided", 1, None),
+                                       (16, 1024, "contiguous-blocks", 0, None),
+                                       (2, 128, "contiguous-blocks", None, 7),
+                                       (8, 32, "strided", None, 3))]
+    for v in variants:
+        for op in ("g[i] += 1", "g[i] = g[i] + 1; if (i < 0) g[0] = 9"):
+            guard.fill(0)
+            ew.ElementwiseKernel("int32_t *g", op, "guard", v, **kwargs)(guard, n=n)
+            got = guard.get()
+            assert np.all(got[:n] == 1) and np.all(got[n:] == 0), (v, op)
+
+
+def test_dot_invariants_and_f64_sum_tolerance(kernel_env):
+    from paper_0911_3456_b200 import reduction as rd
+    import math
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(13)
+    h = rng.standard_normal(257)
+    x = nd.from_host(pool, nd.float64, h)
+    k = rd.dot_kernel(nd.float64, **kwargs)
+    assert k(x, x) >= 0 and k(x, pool.alloc(nd.float64, (257,))) == 0.0
+    big = rng.uniform(-1, 1, 10**6)
+    got = float(rd.sum_kernel(nd.float64, **kwargs)(nd.from_host(pool, nd.float64, big)))
+    exact = math.fsum(big.tolist())
+    assert abs(got - exact) <= 1e-12 * abs(exact) or abs(got - exact) <= 1e-12 * np.abs(big).sum()
