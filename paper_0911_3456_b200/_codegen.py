@@ -21,7 +21,6 @@ pointers and once with register ``rtcg::lane`` wrappers.
 from __future__ import annotations
 
 import ctypes
-import math
 import re
 import struct
 import threading
