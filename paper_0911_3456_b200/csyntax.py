@@ -24,6 +24,7 @@ __all__ = [
     "substitute", "render", "CType", "CNode", "Raw", "Lit", "Ident", "Index",
     "BinOp", "Call", "Assign", "Decl", "Block", "For", "If", "Param",
     "FunctionDef", "TranslationUnit", "counted_for", "emit",
+    "unrolled_add_template", "unrolled_add_ast",
 ]
 
 
@@ -470,3 +471,62 @@ def emit(root: CNode) -> str:
     else:
         raise IllFormedTree("root", f"{type(root).__name__} is not a CNode")
     return "\n".join(lines) + "\n"
+
+
+# --- paper Fig. 4: unrolled vector addition, generated two ways -------------------
+#
+# The reference renders this as host C (src/csyntax.py:535-618); here both
+# strategies emit the same sm_100a kernel: each thread handles `unroll`
+# consecutive elements of a grid-stride walk, with a guarded remainder.
+
+UNROLLED_ADD_CUDA = """\
+extern "C" __global__ void ${name}(const ${ctype} *x, const ${ctype} *y, ${ctype} *z, long n)
+{
+    long i = ((long) blockIdx.x * blockDim.x + threadIdx.x) * ${unroll};
+    const long step = (long) gridDim.x * blockDim.x * ${unroll};
+    for (; i + ${unroll} <= n; i += step) {
+{% for j in 0..unroll %}        z[i + ${j}] = x[i + ${j}] + y[i + ${j}];
+{% endfor %}    }
+{% if unrolled %}    for (long k = i; k < n && k < i + ${unroll}; ++k) {
+        z[k] = x[k] + y[k];
+    }
+{% endif %}}
+"""
+
+
+def unrolled_add_template(unroll: int, ctype: str = "float", name: str = "vadd_unrolled") -> str:
+    """Fig. 4a: the kernel rendered from the text template."""
+    if unroll < 1:
+        raise ValueError("unroll must be at least 1")
+    return render(UNROLLED_ADD_CUDA, {"name": name, "ctype": ctype, "unroll": unroll,
+                                      "unrolled": unroll > 1})
+
+
+def unrolled_add_ast(unroll: int, ctype: str = "float",
+                     name: str = "vadd_unrolled") -> TranslationUnit:
+    """Fig. 4b: the same kernel built as a syntax tree (print with :func:`emit`)."""
+    if unroll < 1:
+        raise ValueError("unroll must be at least 1")
+
+    def at(var: str, j: int) -> CNode:
+        return Ident(var) if j == 0 else BinOp("+", Ident(var), Lit(j))
+
+    def add(var: str, j: int) -> Assign:
+        return Assign(Index(Ident("z"), at(var, j)),
+                      BinOp("+", Index(Ident("x"), at(var, j)), Index(Ident("y"), at(var, j))))
+
+    body: list = [
+        Decl(CType("long"), "i", Raw(f"((long) blockIdx.x * blockDim.x + threadIdx.x) * {unroll}")),
+        Decl(CType("long", const=True), "step", Raw(f"(long) gridDim.x * blockDim.x * {unroll}")),
+        For(None, BinOp("<=", BinOp("+", Ident("i"), Lit(unroll)), Ident("n")),
+            Raw("i += step"), Block(tuple(add("i", j) for j in range(unroll)))),
+    ]
+    if unroll > 1:
+        body.append(For(Decl(CType("long"), "k", Ident("i")),
+                        Raw(f"k < n && k < i + {unroll}"), Raw("++k"), Block((add("k", 0),))))
+    fn = FunctionDef(name, CType("void"),
+                     (Param(CType(ctype, pointer=1, const=True), "x"),
+                      Param(CType(ctype, pointer=1, const=True), "y"),
+                      Param(CType(ctype, pointer=1), "z"), Param(CType("long"), "n")),
+                     Block(tuple(body)), qualifiers='extern "C" __global__')
+    return TranslationUnit((fn,))
