@@ -119,6 +119,10 @@ int rtcg_mem_free(uint64_t dptr);
  * and free are ordered with kernels on `stream` and never synchronise. */
 int rtcg_mem_alloc_async(uint64_t nbytes, rtcg_stream_t stream, uint64_t *dptr);
 int rtcg_mem_free_async(uint64_t dptr, rtcg_stream_t stream);
+/* Synchronise the current device and return the unused memory cached by its
+ * stream-ordered pool to the driver (used before retrying an allocation that
+ * failed with RTCG_ERR_OUT_OF_MEMORY). */
+int rtcg_mem_trim(void);
 int rtcg_memset_async(uint64_t dptr, unsigned char value, uint64_t nbytes,
                       rtcg_stream_t stream);
 int rtcg_memcpy_htod_async(uint64_t dst, const void *src, uint64_t nbytes,

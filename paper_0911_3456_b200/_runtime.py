@@ -130,6 +130,7 @@ _PROTOTYPES = {
     "rtcg_mem_free": (_u64,),
     "rtcg_mem_alloc_async": (_u64, _vp, ctypes.POINTER(_u64)),
     "rtcg_mem_free_async": (_u64, _vp),
+    "rtcg_mem_trim": (),
     "rtcg_memset_async": (_u64, ctypes.c_ubyte, _u64, _vp),
     "rtcg_memcpy_htod_async": (_u64, _vp, _u64, _vp),
     "rtcg_memcpy_dtoh_async": (_vp, _u64, _u64, _vp),
@@ -467,11 +468,21 @@ def launch(function: int, grid: int, block: int, params, smem: int = 0,
 # --- memory ------------------------------------------------------------------------------
 
 
+def _alloc_with_trim(call, what: str) -> None:
+    """Run an allocation; on out-of-memory, trim the stream-ordered pool's
+    cached memory and retry once before raising DeviceOutOfMemory."""
+    status = call()
+    if status == RTCG_ERR_OUT_OF_MEMORY:
+        _check(lib().rtcg_mem_trim(), "trim")
+        status = call()
+    _check(status, what)
+
+
 def mem_alloc(nbytes: int) -> int:
     current_device()
     out = _u64()
-    _check(lib().rtcg_mem_alloc(nbytes, ctypes.byref(out)),
-           f"cuMemAlloc({nbytes})")
+    _alloc_with_trim(lambda: lib().rtcg_mem_alloc(nbytes, ctypes.byref(out)),
+                     f"cuMemAlloc({nbytes})")
     return out.value
 
 
@@ -484,8 +495,8 @@ def mem_alloc_async(nbytes: int, stream=None) -> int:
     current_device()
     s = current_stream() if stream is None else stream
     out = _u64()
-    _check(lib().rtcg_mem_alloc_async(nbytes, s or None, ctypes.byref(out)),
-           f"cuMemAllocAsync({nbytes})")
+    _alloc_with_trim(lambda: lib().rtcg_mem_alloc_async(nbytes, s or None, ctypes.byref(out)),
+                     f"cuMemAllocAsync({nbytes})")
     return out.value
 
 

@@ -77,6 +77,7 @@ struct Driver {
     X(cuMemFreeAsync, CUresult(CUdeviceptr, CUstream))                       \
     X(cuDeviceGetDefaultMemPool, CUresult(CUmemoryPool *, CUdevice))         \
     X(cuMemPoolSetAttribute, CUresult(CUmemoryPool, CUmemPool_attribute, void *)) \
+    X(cuMemPoolTrimTo, CUresult(CUmemoryPool, size_t))                       \
     X(cuMemsetD8Async, CUresult(CUdeviceptr, unsigned char, size_t, CUstream)) \
     X(cuMemcpyHtoDAsync_v2,                                                    \
       CUresult(CUdeviceptr, const void *, size_t, CUstream))               \
@@ -511,6 +512,17 @@ int rtcg_mem_alloc_async(uint64_t nbytes, rtcg_stream_t stream, uint64_t *dptr) 
     CU_CALL(g_drv.cuMemAllocAsync(&p, nbytes, reinterpret_cast<CUstream>(stream)),
             "cuMemAllocAsync");
     *dptr = p;
+    return RTCG_OK;
+}
+
+int rtcg_mem_trim(void) {
+    NEED_CONTEXT();
+    CUdevice dev;
+    CUmemoryPool pool;
+    CU_CALL(g_drv.cuCtxSynchronize(), "cuCtxSynchronize");
+    CU_CALL(g_drv.cuDeviceGet(&dev, t_device), "cuDeviceGet");
+    CU_CALL(g_drv.cuDeviceGetDefaultMemPool(&pool, dev), "cuDeviceGetDefaultMemPool");
+    CU_CALL(g_drv.cuMemPoolTrimTo(pool, 0), "cuMemPoolTrimTo");
     return RTCG_OK;
 }
 

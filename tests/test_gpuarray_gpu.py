@@ -55,3 +55,25 @@ def test_large_blocks_use_stream_ordered_allocation(pool):
     s = pool.stats()
     assert s["bytes_held"] + s["bytes_outstanding"] == s["bytes_from_system"]
     x.free()
+
+
+def test_oom_trims_cached_pool_memory_and_retries(pool):
+    """Fill the device with stream-ordered blocks, free them (they stay cached
+    in the driver pool), then a synchronous allocation of most of the device
+    must still succeed: out-of-memory triggers a trim and one retry."""
+    free, total = _runtime.mem_get_info()
+    chunk = 8 << 30
+    held = []
+    while True:
+        try:
+            held.append(_runtime.mem_alloc_async(chunk))
+        except _runtime.DeviceOutOfMemory:
+            break
+        if len(held) * chunk > total:
+            break
+    assert held
+    for p in held:
+        _runtime.mem_free_async(p)
+    _runtime.synchronize()
+    big = _runtime.mem_alloc(len(held) * chunk - chunk)   # needs the cached memory back
+    _runtime.mem_free(big)
