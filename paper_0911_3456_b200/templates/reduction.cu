@@ -117,11 +117,7 @@ ${smem_loads}
 {% endif %}
 {% if vector %}
 // Vector path: ${unroll} x 16-byte chunks per vector per thread per step,
-// loaded before the fold chains consume them.  Each chunk lane k folds into
-// its own accumulator (E independent chains instead of one; reduce_expr is
-// associative and commutative by contract), and the lanes are folded in
-// order 0..E-1 at the end -- exact for integer/max/min folds, a fixed order
-// (hence bitwise reproducible) for floating point.
+// loaded before the fold chain consumes them.
 extern "C" __global__ void __launch_bounds__(${block})
 ${name}(${kparams_vector}, const long start, const long end,
     ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
@@ -138,9 +134,6 @@ ${unpack}
     };
     rtcg::for_each<1>(sp.lo + sp.first, tl.head_hi, sp.step, elem);
     rtcg::for_each<1>(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
-    ${acc_t} lanes[E];
-#pragma unroll
-    for (int k = 0; k < E; ++k) lanes[k] = RTCG_NEUTRAL;
     for (long c = tl.c_lo + sp.first; c < tl.c_hi; c += U * sp.step) {
 ${vec_decls}
 #pragma unroll
@@ -156,12 +149,10 @@ ${vec_loads}
             if (cu < tl.c_hi) {
 #pragma unroll
                 for (int k = 0; k < E; ++k)
-                    lanes[k] = rtcg_fold(lanes[k], rtcg_map<${lane_types}>(cu * E + k${lane_args}));
+                    acc = rtcg_fold(acc, rtcg_map<${lane_types}>(cu * E + k${lane_args}));
             }
         }
     }
-#pragma unroll
-    for (int k = 0; k < E; ++k) acc = rtcg_fold(acc, lanes[k]);
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
                  [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
 }
