@@ -17,7 +17,7 @@ pool = nd.MemoryPool(device=0)
 N = 1 << 28
 cands = [(1, 128), (1, 256), (1, 512), (2, 128), (2, 256), (4, 128), (4, 256)]
 table = {}
-for dname in ("float32", "float64", "int32", "int64", "int8"):
+for dname in ("float32", "float64", "int32", "int64", "int8", "int16"):
     d = nd.BY_NAME[dname]; c = d.cname
     fill = ew.ElementwiseKernel(f"{c} *x", f"x[i] = ({c}) (i % 100)", f"f_{dname}")
     x = pool.alloc_uninitialized(d, (N,)); y = pool.alloc_uninitialized(d, (N,)); z = pool.alloc_uninitialized(d, (N,))
