@@ -131,6 +131,15 @@ int rtcg_memcpy_dtoh_async(void *dst, uint64_t src, uint64_t nbytes,
                            rtcg_stream_t stream);
 int rtcg_memcpy_dtod_async(uint64_t dst, uint64_t src, uint64_t nbytes,
                            rtcg_stream_t stream);
+/* Host <-> device copies that pick the fast path for the host buffer:
+ * page-locked memory is DMA'd directly (asynchronously); pageable memory is
+ * staged through pinned double buffers, the host-side memcpy parallelised
+ * over worker threads and overlapped with the DMA of the previous chunk.
+ * HtoD returns once `src` may be reused; DtoH returns once `dst` is filled.
+ * (NdArray.copy_from_host / to_host, src/ndarray.py:316-336.) */
+int rtcg_copy_htod(uint64_t dst, const void *src, uint64_t nbytes, rtcg_stream_t stream);
+int rtcg_copy_dtoh(void *dst, uint64_t src, uint64_t nbytes, rtcg_stream_t stream);
+
 /* Page-locked host memory for fast transfers. */
 int rtcg_host_alloc(uint64_t nbytes, void **ptr);
 int rtcg_host_free(void *ptr);

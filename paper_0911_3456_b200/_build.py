@@ -46,7 +46,7 @@ def build_runtime(force: bool = False) -> Path:
         cxx = os.environ.get("CXX") or shutil.which("g++") or "c++"
         tmp = LIB.with_suffix(".so.tmp")
         _run([cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall",
-              f"-I{CUDA_HOME / 'include'}", f"-I{INCLUDE}", str(src), "-ldl",
+              f"-I{CUDA_HOME / 'include'}", f"-I{INCLUDE}", str(src), "-ldl", "-pthread",
               "-o", str(tmp)])
         os.replace(tmp, LIB)
     return LIB

@@ -135,6 +135,8 @@ _PROTOTYPES = {
     "rtcg_memcpy_htod_async": (_u64, _vp, _u64, _vp),
     "rtcg_memcpy_dtoh_async": (_vp, _u64, _u64, _vp),
     "rtcg_memcpy_dtod_async": (_u64, _u64, _u64, _vp),
+    "rtcg_copy_htod": (_u64, _vp, _u64, _vp),
+    "rtcg_copy_dtoh": (_vp, _u64, _u64, _vp),
     "rtcg_host_alloc": (_u64, ctypes.POINTER(_vp)),
     "rtcg_host_free": (_vp,),
     "rtcg_host_register": (_vp, _u64),
@@ -518,6 +520,18 @@ def memcpy_htod(dst: int, src: int, nbytes: int, stream=None) -> None:
 def memcpy_dtoh(dst: int, src: int, nbytes: int, stream=None) -> None:
     s = current_stream() if stream is None else stream
     _check(lib().rtcg_memcpy_dtoh_async(dst, src, nbytes, s or None), "DtoH")
+
+
+def copy_htod(dst: int, src: int, nbytes: int, stream=None) -> None:
+    """Host->device copy; pageable sources go through pinned staging."""
+    s = current_stream() if stream is None else stream
+    _check(lib().rtcg_copy_htod(dst, src, nbytes, s or None), "HtoD")
+
+
+def copy_dtoh(dst: int, src: int, nbytes: int, stream=None) -> None:
+    """Device->host copy into pinned or pageable memory; returns when filled."""
+    s = current_stream() if stream is None else stream
+    _check(lib().rtcg_copy_dtoh(dst, src, nbytes, s or None), "DtoH")
 
 
 def memcpy_dtod(dst: int, src: int, nbytes: int, stream=None) -> None:

@@ -16,13 +16,21 @@
 #include <cuda.h>
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
+
+#include <unistd.h>
+#if defined(__x86_64__)
+#include <emmintrin.h>
+#endif
 
 namespace {
 
@@ -88,6 +96,7 @@ struct Driver {
     X(cuMemFreeHost, CUresult(void *))                                     \
     X(cuMemHostRegister_v2, CUresult(void *, size_t, unsigned))            \
     X(cuMemHostUnregister, CUresult(void *))                               \
+    X(cuMemHostGetFlags, CUresult(unsigned *, void *))                     \
     X(cuStreamCreate, CUresult(CUstream *, unsigned))                      \
     X(cuStreamDestroy_v2, CUresult(CUstream))                              \
     X(cuStreamSynchronize, CUresult(CUstream))                             \
@@ -558,6 +567,253 @@ int rtcg_memcpy_dtod_async(uint64_t dst, uint64_t src, uint64_t nbytes, rtcg_str
     CU_CALL(g_drv.cuMemcpyDtoDAsync_v2(dst, src, nbytes, reinterpret_cast<CUstream>(stream)),
             "cuMemcpyDtoDAsync");
     return RTCG_OK;
+}
+
+// ---------------------------------------------------------------- staged copies
+//
+// Pageable host memory cannot be DMA'd; the driver stages it through a small
+// bounce buffer with one thread (~11 GB/s HtoD on the B200 box).  The copy
+// engine instead splits a transfer into one contiguous slice per worker
+// thread; every worker owns two pinned lane buffers and pipelines
+//   HtoD: host memcpy (non-temporal stores) into lane buffer -> async DMA
+//   DtoH: async DMA into lane buffer -> host memcpy out of it
+// on the caller's stream, so host-side copying (the bound: host DRAM) runs on
+// many cores while the DMA engine stays busy.  One engine per device, created
+// on first use, workers persistent; calls are serialised per engine.
+
+namespace {
+
+constexpr size_t kLaneBytes = 4u << 20;     // per lane buffer (2 per worker)
+constexpr size_t kDirectBelow = 1u << 20;   // small copies: let the driver stage
+
+// 64-byte blocks of 16-byte non-temporal stores: no read-for-ownership of
+// the destination, which would otherwise add a third pass over host DRAM
+void stream_copy(void *dst, const void *src, size_t n) {
+#if defined(__x86_64__)
+    static const bool nt = [] {
+        const char *env = getenv("RTCG_COPY_NT");
+        return !(env && env[0] == '0');
+    }();
+    char *d = static_cast<char *>(dst);
+    const char *s = static_cast<const char *>(src);
+    if (!nt || n < 4096) {
+        memcpy(d, s, n);
+        return;
+    }
+    const size_t head = (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+    memcpy(d, s, head);
+    d += head, s += head, n -= head;
+    const size_t body = n & ~size_t(63);
+    for (size_t i = 0; i < body; i += 64) {
+        __m128i x0 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i));
+        __m128i x1 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 16));
+        __m128i x2 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 32));
+        __m128i x3 = _mm_loadu_si128(reinterpret_cast<const __m128i *>(s + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i *>(d + i), x0);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 16), x1);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 32), x2);
+        _mm_stream_si128(reinterpret_cast<__m128i *>(d + i + 48), x3);
+    }
+    _mm_sfence();
+    memcpy(d + body, s + body, n - body);
+#else
+    memcpy(dst, src, n);
+#endif
+}
+
+bool is_pinned(const void *p) {
+    unsigned flags = 0;
+    return g_drv.cuMemHostGetFlags(&flags, const_cast<void *>(p)) == CUDA_SUCCESS;
+}
+
+struct CopyJob {
+    bool to_device = true;
+    uint64_t dev = 0;
+    char *host = nullptr;
+    uint64_t nbytes = 0;
+    size_t slice = 0;
+    CUstream stream = nullptr;
+};
+
+struct Lane {
+    void *buf[2] = {};
+    CUevent done[2] = {};
+    CUresult err = CUDA_SUCCESS;
+    const char *what = "";
+};
+
+class CopyEngine {
+  public:
+    CopyEngine(CUcontext ctx, unsigned workers) : ctx_(ctx), lanes_(workers), pid_(getpid()) {}
+
+    int start() {
+        for (auto &lane : lanes_)
+            for (int b = 0; b < 2; ++b) {
+                CU_CALL(g_drv.cuMemHostAlloc(&lane.buf[b], kLaneBytes, CU_MEMHOSTALLOC_PORTABLE),
+                        "cuMemHostAlloc(copy lane)");
+                CU_CALL(g_drv.cuEventCreate(&lane.done[b], CU_EVENT_DISABLE_TIMING),
+                        "cuEventCreate(copy lane)");
+            }
+        for (unsigned w = 1; w < lanes_.size(); ++w)
+            std::thread([this, w] { worker(w); }).detach();  // engine lives for the process
+        return RTCG_OK;
+    }
+
+    bool forked() const { return getpid() != pid_; }
+
+    int run(const CopyJob &job) {
+        std::lock_guard<std::mutex> call(call_mutex_);
+        const unsigned active = (unsigned)std::min<uint64_t>(
+            lanes_.size(), (job.nbytes + kLaneBytes - 1) / kLaneBytes);
+        {
+            std::lock_guard<std::mutex> lock(m_);
+            job_ = job;
+            job_.slice = ((job.nbytes + active - 1) / active + 63) & ~size_t(63);
+            active_ = active;
+            pending_ = active - 1;
+            ++generation_;
+        }
+        wake_.notify_all();
+        run_lane(0);
+        std::unique_lock<std::mutex> lock(m_);
+        done_.wait(lock, [this] { return pending_ == 0; });
+        for (unsigned w = 0; w < active; ++w)
+            if (lanes_[w].err != CUDA_SUCCESS) return cu_fail(lanes_[w].err, lanes_[w].what);
+        return RTCG_OK;
+    }
+
+  private:
+    void worker(unsigned w) {
+        g_drv.cuCtxSetCurrent(ctx_);
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lock(m_);
+                wake_.wait(lock, [&] { return generation_ != seen; });
+                seen = generation_;
+                if (w >= active_) continue;
+            }
+            run_lane(w);
+            std::lock_guard<std::mutex> lock(m_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+
+#define LANE_CALL(expr, name)                  \
+    do {                                       \
+        CUresult r_ = (expr);                  \
+        if (r_ != CUDA_SUCCESS) {              \
+            lane.err = r_, lane.what = name;   \
+            return;                            \
+        }                                      \
+    } while (0)
+
+    void run_lane(unsigned w) {
+        Lane &lane = lanes_[w];
+        lane.err = CUDA_SUCCESS;
+        const CopyJob &job = job_;
+        const uint64_t lo = std::min<uint64_t>(job.nbytes, w * job.slice);
+        const uint64_t hi = std::min<uint64_t>(job.nbytes, lo + job.slice);
+        const uint64_t chunks = (hi - lo + kLaneBytes - 1) / kLaneBytes;
+        auto len = [&](uint64_t k) { return (size_t)std::min<uint64_t>(kLaneBytes, hi - lo - k * kLaneBytes); };
+        if (job.to_device) {
+            for (uint64_t k = 0; k < chunks; ++k) {
+                const int b = k & 1;
+                const uint64_t off = lo + k * kLaneBytes;
+                LANE_CALL(g_drv.cuEventSynchronize(lane.done[b]), "cuEventSynchronize(copy lane)");
+                stream_copy(lane.buf[b], job.host + off, len(k));
+                LANE_CALL(g_drv.cuMemcpyHtoDAsync_v2(job.dev + off, lane.buf[b], len(k), job.stream),
+                          "cuMemcpyHtoDAsync(staged)");
+                LANE_CALL(g_drv.cuEventRecord(lane.done[b], job.stream), "cuEventRecord(copy lane)");
+            }
+            return;  // the host slice is no longer referenced; DMA may be in flight
+        }
+        auto issue = [&](uint64_t k) -> CUresult {
+            const int b = k & 1;
+            CUresult r = g_drv.cuEventSynchronize(lane.done[b]);  // earlier user of buf[b]
+            if (r == CUDA_SUCCESS)
+                r = g_drv.cuMemcpyDtoHAsync_v2(lane.buf[b], job.dev + lo + k * kLaneBytes, len(k),
+                                               job.stream);
+            if (r == CUDA_SUCCESS) r = g_drv.cuEventRecord(lane.done[b], job.stream);
+            return r;
+        };
+        if (chunks) LANE_CALL(issue(0), "cuMemcpyDtoHAsync(staged)");
+        for (uint64_t k = 0; k < chunks; ++k) {
+            if (k + 1 < chunks) LANE_CALL(issue(k + 1), "cuMemcpyDtoHAsync(staged)");
+            const int b = k & 1;
+            LANE_CALL(g_drv.cuEventSynchronize(lane.done[b]), "cuEventSynchronize(copy lane)");
+            stream_copy(job.host + lo + k * kLaneBytes, lane.buf[b], len(k));
+        }
+    }
+#undef LANE_CALL
+
+    CUcontext ctx_;
+    std::vector<Lane> lanes_;
+    pid_t pid_;
+    std::mutex call_mutex_, m_;
+    std::condition_variable wake_, done_;
+    CopyJob job_;
+    uint64_t generation_ = 0;
+    unsigned active_ = 0, pending_ = 0;
+};
+
+std::mutex g_engine_mutex;
+std::vector<CopyEngine *> g_engines;  // per device, leaked at exit on purpose
+
+int copy_engine(CopyEngine *&out) {
+    std::lock_guard<std::mutex> lock(g_engine_mutex);
+    if ((int)g_engines.size() <= t_device) g_engines.resize(t_device + 1, nullptr);
+    CopyEngine *&e = g_engines[t_device];
+    if (!e || e->forked()) {  // a forked child has none of the parent's workers
+        CUcontext ctx = nullptr;
+        CU_CALL(g_drv.cuCtxGetCurrent(&ctx), "cuCtxGetCurrent");
+        static const unsigned workers = [] {
+            const char *env = getenv("RTCG_COPY_THREADS");  // probing knob
+            unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+            return env && atoi(env) > 0 ? (unsigned)atoi(env) : std::min(hw, 8u);  // 8: measured best
+        }();
+        auto *fresh = new CopyEngine(ctx, workers);
+        int st = fresh->start();
+        if (st != RTCG_OK) return st;  // partially set up engine leaks; rare
+        e = fresh;
+    }
+    out = e;
+    return RTCG_OK;
+}
+
+}  // namespace
+
+int rtcg_copy_htod(uint64_t dst, const void *src, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CUstream s = reinterpret_cast<CUstream>(stream);
+    if (nbytes < kDirectBelow || is_pinned(src)) {
+        CU_CALL(g_drv.cuMemcpyHtoDAsync_v2(dst, src, nbytes, s), "cuMemcpyHtoDAsync");
+        return RTCG_OK;
+    }
+    CopyEngine *e = nullptr;
+    int st = copy_engine(e);
+    if (st != RTCG_OK) return st;
+    CopyJob job;
+    job.to_device = true, job.dev = dst, job.host = const_cast<char *>(static_cast<const char *>(src));
+    job.nbytes = nbytes, job.stream = s;
+    return e->run(job);
+}
+
+int rtcg_copy_dtoh(void *dst, uint64_t src, uint64_t nbytes, rtcg_stream_t stream) {
+    NEED_CONTEXT();
+    CUstream s = reinterpret_cast<CUstream>(stream);
+    if (nbytes < kDirectBelow || is_pinned(dst)) {
+        CU_CALL(g_drv.cuMemcpyDtoHAsync_v2(dst, src, nbytes, s), "cuMemcpyDtoHAsync");
+        CU_CALL(g_drv.cuStreamSynchronize(s), "cuStreamSynchronize");
+        return RTCG_OK;
+    }
+    CopyEngine *e = nullptr;
+    int st = copy_engine(e);
+    if (st != RTCG_OK) return st;
+    CopyJob job;
+    job.to_device = false, job.dev = src, job.host = static_cast<char *>(dst);
+    job.nbytes = nbytes, job.stream = s;
+    return e->run(job);
 }
 
 int rtcg_host_alloc(uint64_t nbytes, void **ptr) {
