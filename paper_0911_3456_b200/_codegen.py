@@ -42,9 +42,9 @@ CACHE_POLICIES = {
     "default": (1, 0, 0),
     "streaming": (2, 2, 1),
     "no-l1": (3, 0, 2),
-    # reductions: read-only inputs staged through shared memory by TMA bulk
-    # copies (templates/reduction.cu "TMA path"); elementwise kernels treat it
-    # as "default"
+    # inputs staged through shared memory by TMA bulk copies (the "TMA path"
+    # of templates/reduction.cu and templates/elementwise.cu); the policies
+    # apply to the pointer-path head/tail and to elementwise stores
     "tma": (1, 0, 0),
 }
 TMA_STAGES = 4
@@ -52,13 +52,27 @@ TMA_STAGE_BYTES = 32 * 1024
 TMA_HEADER = 128
 
 
-def tma_parts(sig, access, width: int) -> dict:
-    """Bindings of the reduction template's TMA path: ring buffers (one per
-    used vector), bulk copies, shared-memory chunk loads and the dynamic
-    shared-memory size."""
-    used = [p for p in sig.vectors if access[p.name].used]
+def tma_parts(sig, access, width: int, block: int | None = None,
+              staged: str = "used") -> dict:
+    """Bindings of a template's TMA path: shared-memory rings (one per staged
+    vector), the producer's bulk copies, the consumers' shared-memory chunk
+    loads and the dynamic shared-memory size.
+
+    Reductions stage every used vector (``staged="used"``) in 32 KB-ish tiles.
+    Elementwise kernels stage the vectors they *read* (``staged="read"``;
+    written vectors are stored straight from registers) and size the tile so
+    every consumer thread (all warps but the producer) owns the same number of
+    16-byte chunks -- an uneven split idles consumers on compute-heavy
+    statements."""
+    pick = (lambda a: a.used) if staged == "used" else (lambda a: a.read)
+    used = [p for p in sig.vectors if pick(access[p.name])]
     per_elem = sum(p.dtype.size for p in used)
-    tile = max(width * 16, (TMA_STAGE_BYTES // per_elem) // width * width)
+    if block is None:
+        tile = max(width * 16, (TMA_STAGE_BYTES // per_elem) // width * width)
+    else:
+        consumers = block - 32
+        per_thread = max(1, TMA_STAGE_BYTES // (consumers * width * per_elem))
+        tile = per_thread * consumers * width
     rings, bulks, loads = [], [], []
     offset = 0
     for p in used:
@@ -72,6 +86,12 @@ def tma_parts(sig, access, width: int) -> dict:
     return {"tma": True, "stages": TMA_STAGES, "tile": tile, "tile_bytes": tile * per_elem,
             "ring_decls": "\n".join(rings), "bulk_loads": "\n".join(bulks),
             "smem_loads": "\n".join(loads), "tma_smem": TMA_HEADER + offset}
+
+
+def tma_eligible(sig, access, width: int) -> bool:
+    """An elementwise TMA path needs the vector path and something to stage."""
+    return (access is not None and width > 0
+            and any(access[p.name].read for p in sig.vectors))
 
 _CONTROL = re.compile(r"\b(?:if|else|for|while|do|switch|case|goto|return|break|continue)\b|[{}]")
 

@@ -66,3 +66,80 @@ ${vec_stores}
     }
 }
 {% endif %}
+{% if tma %}
+// TMA path: a producer warp streams ${stages} ring stages of ${tile}-element
+// tiles of every vector the statement reads into shared memory with 1-D bulk
+// copies (cp.async.bulk, completion counted in bytes on a "full" mbarrier),
+// so loads stay in flight while the consumer warps compute.  Each consumer
+// thread takes the same number of 16-byte chunks of a tile from shared
+// memory, runs the statement on registers, stores written vectors straight
+// to HBM and hands the stage back through an "empty" mbarrier.  Tiles b,
+// b+G, b+2G... belong to CTA b; elements outside whole tiles take the
+// pointer path.
+extern "C" __global__ void __launch_bounds__(${block})
+${name}(${kparams_vector}, const long start, const long end)
+{
+${unpack}
+    constexpr int E = ${width};
+    constexpr int U = 1;
+    constexpr int S = ${stages};
+    constexpr long TE = ${tile};
+    extern __shared__ __align__(128) unsigned char rtcg_smem[];
+    unsigned long long *rtcg_full = reinterpret_cast<unsigned long long *>(rtcg_smem);
+    unsigned long long *rtcg_empty = rtcg_full + S;
+    unsigned char *rtcg_ring = rtcg_smem + 128;
+${ring_decls}
+    const int warp = threadIdx.x >> 5, lane_id = threadIdx.x & 31;
+    const int consumers = (int)(blockDim.x >> 5) - 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            rtcg::tma::mbar_init(rtcg_full + s, 1);
+            rtcg::tma::mbar_init(rtcg_empty + s, (unsigned)consumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto elem = [&](const long i) { rtcg_op<${ptr_types_vector}>(i${call_args}); };
+    const long t_lo = (start + TE - 1) / TE, t_hi = end / TE;
+    const long G = gridDim.x, b = blockIdx.x;
+    const long gtid = b * (long)blockDim.x + threadIdx.x, gstep = G * (long)blockDim.x;
+    if (t_lo >= t_hi) {
+        rtcg::for_each<1>(start + gtid, end, gstep, elem);
+        return;
+    }
+    rtcg::for_each<1>(start + gtid, t_lo * TE, gstep, elem);
+    rtcg::for_each<1>(t_hi * TE + gtid, end, gstep, elem);
+    const long mine = b < t_hi - t_lo ? (t_hi - t_lo - b + G - 1) / G : 0;
+    if (warp == 0) {
+        if (lane_id == 0) {
+            for (long j = 0; j < mine; ++j) {
+                const int s = (int)(j % S);
+                if (j >= S) rtcg::tma::mbar_wait(rtcg_empty + s, (unsigned)(((j / S) - 1) & 1));
+                const long t = t_lo + b + j * G;
+                rtcg::tma::mbar_expect_tx(rtcg_full + s, ${tile_bytes}u);
+${bulk_loads}
+            }
+        }
+    } else {
+        const long ct = threadIdx.x - 32, cn = (long)consumers * 32;
+        for (long j = 0; j < mine; ++j) {
+            const int s = (int)(j % S);
+            rtcg::tma::mbar_wait(rtcg_full + s, (unsigned)((j / S) & 1));
+            const long t = t_lo + b + j * G;
+#pragma unroll 1
+            for (long c = ct; c < TE / E; c += cn) {
+                const long cu = t * (TE / E) + c;
+                constexpr int u = 0;
+${vec_decls}
+${smem_loads}
+#pragma unroll
+                for (int k = 0; k < E; ++k)
+                    rtcg_op<${lane_types}>(cu * E + k${lane_args});
+${vec_stores}
+            }
+            __syncwarp();
+            if (lane_id == 0) rtcg::tma::mbar_arrive(rtcg_empty + s);
+        }
+    }
+}
+{% endif %}

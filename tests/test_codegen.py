@@ -62,7 +62,7 @@ _ident = st.from_regex(r"[a-hj-mo-qs-z][a-z0-9_]{0,5}", fullmatch=True).filter(
                 min_size=1, max_size=6, unique_by=lambda t: t[0]))
 def test_parse_round_trips_generated_signatures(params):
     if not any(vec for _, _, vec in params):
-        params = params + [("zz", "float", True)]
+        params = params + [("rv", "float", True)]  # "r..." is never drawn by _ident
     text = ", ".join(f"{c} {'*' if v else ''}{n}" for n, c, v in params)
     sig = ew.parse_signature(text)
     assert ew.parse_signature(sig.render()) == sig and len(sig.params) == len(params)
@@ -239,3 +239,15 @@ def test_c_math_semantics_in_prelude(nvrtc_cache, tmp_path):
                       ew.VariantParams())
     sass = _sass(jit.compile(src, cache=nvrtc_cache).image, tmp_path)
     assert "F2F.F64.F32" in sass and "DFMA" in sass
+
+
+def test_elementwise_tma_entry_uses_bulk_copies():
+    from paper_0911_3456_b200 import _codegen as cg, elementwise as ew
+    src = ew.generate(ew.parse_signature("double *x, double *z"), "z[i] = x[i];", "cp",
+                      ew.VariantParams(cache="tma"))
+    assert "cp.async.bulk" in src and "rtcg_full" in src
+    assert cg.tma_eligible(ew.parse_signature("double *x, double *z"),
+                           cg.analyze("z[i] = x[i];", ["x", "z"]), 2)
+    with pytest.raises(ValueError):
+        ew.generate(ew.parse_signature("double *x, double *z"), "z[i] = x[i];", "cp",
+                    ew.VariantParams(cache="tma", block=32))

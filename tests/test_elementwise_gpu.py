@@ -26,7 +26,8 @@ def digest(a):
 _VARIANTS = (ew.VariantParams(unroll=1, block=128, chunking="contiguous-blocks"),
              ew.VariantParams(unroll=4, block=256),
              ew.VariantParams(unroll=8, block=512, workers=3, chunking="contiguous-blocks"),
-             ew.VariantParams(unroll=2, block=64, workers=5))
+             ew.VariantParams(unroll=2, block=64, workers=5),
+             ew.VariantParams(cache="tma", block=128, workers=3))
 
 
 @pytest.mark.parametrize("dname", csem.DTYPE_NAMES)
@@ -439,6 +440,8 @@ def test_partition_covers_every_index_exactly_once(kernel_env, n):
                                        (16, 1024, "contiguous-blocks", 0, None),
                                        (2, 128, "contiguous-blocks", None, 7),
                                        (8, 32, "strided", None, 3))]
+    variants += [ew.VariantParams(cache="tma", block=b, waves=w, workers=wk)
+                 for b, w, wk in ((256, None, None), (64, None, 2), (1024, 2, None))]
     for v in variants:
         for op in ("g[i] += 1", "g[i] = g[i] + 1; if (i < 0) g[0] = 9"):
             guard.fill(0)
