@@ -79,7 +79,7 @@ def tma_parts(sig, access, width: int, block: int | None = None,
         c = p.dtype.cname
         rings.append(f"    {c} *rtcg_r_{p.name} = reinterpret_cast<{c} *>(rtcg_ring + {offset});")
         bulks.append(f"                    rtcg::tma::bulk_load(rtcg_r_{p.name} + s * TE, "
-                     f"{p.name} + t * TE, (unsigned)(TE * sizeof({c})), rtcg_full + s);")
+                     f"rtcg_p_{p.name} + t * TE, (unsigned)(TE * sizeof({c})), rtcg_full + s);")
         loads.append(f"                    rtcg::tma::load_smem(rtcg_v_{p.name}[u], "
                      f"rtcg_r_{p.name} + s * TE, c);")
         offset += TMA_STAGES * tile * p.dtype.size
@@ -159,7 +159,14 @@ def chunk_width(sig, access) -> int:
 
 
 def parts(sig, access, width: int, policy: str) -> dict:
-    """Placeholder bindings shared by the elementwise and reduction templates."""
+    """Placeholder bindings shared by the elementwise and reduction templates.
+
+    User identifiers never appear in kernel scope: kernel parameters are
+    ``rtcg_p_<name>`` (vectors) / ``rtcg_w_<name>`` (widened scalars), the
+    converted scalars ``rtcg_s_<name>``; the user's names exist only as the
+    parameters of ``rtcg_op`` / ``rtcg_map``.  So a parameter called ``b``,
+    ``k`` or ``E`` cannot collide with, or be shadowed by, template locals
+    (``rtcg_`` is a reserved prefix)."""
     ld_ro, ld_rw, st = CACHE_POLICIES[policy]
     vec_ok = access is not None and width > 0
     op_tparams, op_params, kgen, kvec, unpack = [], [], [], [], []
@@ -167,23 +174,24 @@ def parts(sig, access, width: int, policy: str) -> dict:
     decls, loads, stores = [], [], []
     for p in sig.params:
         c = p.dtype.cname
-        call_args.append(f", {p.name}")
         if not p.is_vector:
             wide = _WIDE[p.dtype.kind][0]
             op_params.append(f", {c} {p.name}")
             kgen.append(f"{wide} rtcg_w_{p.name}")
             kvec.append(f"{wide} rtcg_w_{p.name}")
-            unpack.append(f"    {c} {p.name} = ({c}) rtcg_w_{p.name};")
-            lane_args.append(f", {p.name}")
+            unpack.append(f"    const {c} rtcg_s_{p.name} = ({c}) rtcg_w_{p.name};")
+            call_args.append(f", rtcg_s_{p.name}")
+            lane_args.append(f", rtcg_s_{p.name}")
             continue
+        call_args.append(f", rtcg_p_{p.name}")
         op_tparams.append(f"class rtcg_T_{p.name}")
         op_params.append(f", rtcg_T_{p.name} {p.name}")
-        kgen.append(f"{c} *{p.name}")
+        kgen.append(f"{c} *rtcg_p_{p.name}")
         ptr_gen.append(f"{c} *")
         acc = access[p.name] if vec_ok else Access(True, True)
         read_only = acc.read and not acc.written
         qual = "const " if read_only else ""
-        kvec.append(f"{qual}{c} *__restrict__ {p.name}")
+        kvec.append(f"{qual}{c} *__restrict__ rtcg_p_{p.name}")
         ptr_vec.append(f"{qual}{c} *")
         if vec_ok and acc.used:
             lane_types.append(f"rtcg::lane<{c}>")
@@ -191,12 +199,12 @@ def parts(sig, access, width: int, policy: str) -> dict:
             decls.append(f"        rtcg::chunk<{c}, E> rtcg_v_{p.name}[U];")
             if acc.read:
                 hint = ld_ro if read_only else ld_rw
-                loads.append(f"                rtcg::load<{hint}>(rtcg_v_{p.name}[u], {p.name}, cu);")
+                loads.append(f"                rtcg::load<{hint}>(rtcg_v_{p.name}[u], rtcg_p_{p.name}, cu);")
             if acc.written:
-                stores.append(f"                rtcg::store<{st}>({p.name}, cu, rtcg_v_{p.name}[u]);")
+                stores.append(f"                rtcg::store<{st}>(rtcg_p_{p.name}, cu, rtcg_v_{p.name}[u]);")
         else:
             lane_types.append(f"{qual}{c} *")
-            lane_args.append(f", {p.name}")
+            lane_args.append(f", rtcg_p_{p.name}")
     return {
         "vector": vec_ok,
         "tma": False,

@@ -251,3 +251,20 @@ def test_elementwise_tma_entry_uses_bulk_copies():
     with pytest.raises(ValueError):
         ew.generate(ew.parse_signature("double *x, double *z"), "z[i] = x[i];", "cp",
                     ew.VariantParams(cache="tma", block=32))
+
+
+# User parameter names that are also template locals (loop counters, tile
+# bookkeeping, C-ish one-letter names) must neither collide nor be shadowed.
+_CLASH_SIG = "float k, float *c, double E, float *b, float *s"
+_CLASH_OP = "s[i] = k * c[i] + (float) E * b[i]"
+
+
+@pytest.mark.parametrize("cache", ["default", "tma"])
+def test_template_locals_never_clash_with_user_names(nvrtc_cache, cache):
+    from paper_0911_3456_b200 import jit
+    v = ew.VariantParams(cache=cache, unroll=2)
+    src = ew.generate(ew.parse_signature(_CLASH_SIG), _CLASH_OP + ";", "clash", v)
+    jit.compile(src, cache=nvrtc_cache)
+    spec = rd.ReductionSpec("float *b, long G, float *t", nd.float64, "0", "a + b",
+                            "b[i] * t[i] + G")
+    jit.compile(rd.generate_reduction_source(spec, "clash_r", v), cache=nvrtc_cache)

@@ -134,3 +134,21 @@ def test_write_only_statement_has_no_tma_entry(kernel_env):
     z = pool.alloc(nd.float32, (1001,))
     k(z)
     assert np.all(z.to_host() == 1.5)
+
+
+@pytest.mark.parametrize("cache", ["default", "tma"])
+def test_user_names_that_match_template_locals(kernel_env, cache):
+    """A scalar called ``k`` used to be shadowed by the chunk loop counter on
+    the vector path (silently wrong values); names are now namespaced."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(8)
+    n = 100_003
+    c = rng.uniform(-1, 1, n).astype(np.float32)
+    b = rng.uniform(-1, 1, n).astype(np.float32)
+    k = ew.make_elementwise("float k, float *c, double E, float *b, float *s",
+                            "s[i] = k * c[i] + (float) E * b[i]", "clash",
+                            ew.VariantParams(cache=cache, unroll=2), **kwargs)
+    gc, gb, gs = (nd.from_host(pool, nd.float32, c), nd.from_host(pool, nd.float32, b),
+                  pool.alloc(nd.float32, (n,)))
+    k(1.25, gc, -0.5, gb, gs)
+    assert np.array_equal(gs.to_host(), np.float32(1.25) * c + np.float32(-0.5) * b)
