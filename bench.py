@@ -461,7 +461,9 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
            note="values in [-2^62, 2^62): the sum wraps (bit-exact, order independent)")
     xi.free()
 
-    xd = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
+    hx = nd.pinned_empty((n,), nd.float64)
+    hx[:] = rng.uniform(-2, 2, n)
+    xd = nd.from_host(pool, nd.float64, hx)
     zd = pool.alloc_uninitialized(nd.float64, (n,))
     sig, op = ("double a, double *x, double *z",
                "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
@@ -469,7 +471,46 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
                             protocol=proto, store=store)
     ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**t.best_assignment))
     record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n, t,
-           bound="fp64 issue (double sin: ~37 DP instructions/element), not HBM")
+           bound="instruction issue + HBM: ~67 instructions/element (~21 FP64); ncu: issue "
+                 "slots 68% busy, FP64 pipe 44%, DRAM 68.5% (profiles/r01_ncu_full_polysin_*)")
+    # C3 end to end through the public API: pinned host x -> HBM, kernel, HBM ->
+    # pinned host z (16 B/element cross the host link), against the reference's
+    # CPU kernel on all host cores -- the compute-heavy case where the GPU wins
+    # end to end even though every byte crosses PCIe.
+    hz = nd.pinned_empty((n,), nd.float64)
+
+    def e2e():
+        xd.copy_from_host(hx, sync=False)
+        ps(0.5, xd, zd)
+        zd.to_host(out=hz)
+    e2e()
+    reps = 3
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        e2e()
+    e2e_s = (time.perf_counter() - t0) / reps
+    out["polysin_f64_2p28"]["e2e"] = {
+        "value": round(16 * n / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+        "d2h_bytes_per_step": 8 * n, "steps": reps,
+        "path": "GPUArray.copy_from_host (pinned) + ElementwiseKernel + GPUArray.to_host (pinned)"}
+    try:
+        from oracle import refdrive
+        fn, kind = refdrive.load("polysin")
+        threads = refdrive.host_threads()
+        m = 1 << 23
+        cx, cz = np.ascontiguousarray(hx[:m]), np.empty(m)
+        fn(0.5, cx, cz, workers=threads)
+        best = math.inf
+        for _ in range(5):
+            t0 = time.perf_counter()
+            fn(0.5, cx, cz, workers=threads)
+            best = min(best, time.perf_counter() - t0)
+        out["polysin_f64_2p28"]["cpu_baseline"] = {
+            "value": round(16 * m / best / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": kind, "sample": f"polysin f64 n=2^23 (bounded sample), x~U(-2,2), "
+                                    f"reference variant, {threads} worker threads, best of 5"}
+    except Exception as exc:  # pragma: no cover - report, don't fail the bench
+        out["polysin_f64_2p28"]["cpu_baseline"] = {"value": None, "error": str(exc)}
     xd.free()
     zd.free()
     return out

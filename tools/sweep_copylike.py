@@ -23,6 +23,10 @@ def mean_ms(fn, reps=10):
     return s.elapsed_ms(e) / reps
 
 
+import os  # noqa: E402
+from paper_0911_3456_b200 import _codegen as cg  # noqa: E402
+if os.environ.get("TMA_STAGE_BYTES"):
+    cg.TMA_STAGE_BYTES = int(os.environ["TMA_STAGE_BYTES"])
 rt.set_device(0)
 pool = nd.MemoryPool(device=0)
 n = 1 << 28
@@ -30,8 +34,9 @@ x = nd.from_host(pool, nd.float64, np.random.default_rng(1).uniform(-2, 2, n))
 z = pool.alloc_uninitialized(nd.float64, (n,))
 ops = {"copy": "z[i] = x[i]", "poly": "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i]",
        "polysin": "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])"}
-only = sys.argv[1:] or list(ops)
-caches = ("default", "tma") if "--tma" in sys.argv else ("default",)
+only = [a for a in sys.argv[1:] if not a.startswith("--")] or list(ops)
+caches = ("tma",) if "--tma-only" in sys.argv else \
+    ("default", "tma") if "--tma" in sys.argv else ("default",)
 rows = []
 for name in [o for o in ops if o in only]:
     op = ops[name]
@@ -49,4 +54,4 @@ for name in [o for o in ops if o in only]:
     for r in best:
         print(json.dumps(r), flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
-Path("gpurun_out/sweep_copylike.json").write_text(json.dumps(rows, indent=1))
+Path(f"gpurun_out/sweep_copylike{os.environ.get('TMA_STAGE_BYTES', '')}.json").write_text(json.dumps(rows, indent=1))
