@@ -336,7 +336,7 @@ def test_adaptive_kernels(kernel_env):
     y = nd.from_host(pool, nd.float32, np.full(4, 0.5, np.float32))
     k = ew.make_elementwise_adaptive([("x", x), ("y", y)], "out[i] = x[i] + y[i]",
                                      "ada_mix", **kwargs)
-    assert k.result_dtype is nd.float64 and "float *y" in k.source
+    assert k.result_dtype is nd.float64 and "float *y" in k.signature.render()
     out = pool.alloc(nd.float64, (4,))
     k(x, y, out)
     assert list(out.to_host()) == [1.5, 2.5, 3.5, 4.5]
