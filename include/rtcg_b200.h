@@ -165,6 +165,19 @@ int rtcg_stream_end_capture(rtcg_stream_t stream, rtcg_graph_t *graph);
 int rtcg_graph_launch(rtcg_graph_t graph, rtcg_stream_t stream);
 int rtcg_graph_destroy(rtcg_graph_t graph);
 
+/* --- peer memory (no reference equivalent: the reference's workers share one
+ * address space).  The multi-GPU reduction exchanges its per-GPU accumulators
+ * inside the reduction kernel itself, with stores into every peer's mailbox
+ * over NVLink / NVSwitch (parallel.PeerMailbox; replaces the ordered host fold
+ * of worker partials, src/reduction.py:211-216, at GPU granularity).
+ * Mailboxes are rtcg_mem_alloc buffers shared across the one-process-per-GPU
+ * ranks with CUDA IPC handles (64 opaque bytes). */
+int rtcg_ipc_get_handle(uint64_t dptr, unsigned char handle[64]);
+/* Maps a peer process's buffer (peer access enabled lazily). */
+int rtcg_ipc_open_handle(const unsigned char handle[64], uint64_t *dptr);
+int rtcg_ipc_close_handle(uint64_t dptr);
+int rtcg_device_can_access_peer(int device, int peer, int *can);
+
 #ifdef __cplusplus
 }
 #endif

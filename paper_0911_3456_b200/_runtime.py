@@ -153,6 +153,10 @@ _PROTOTYPES = {
     "rtcg_stream_end_capture": (_vp, ctypes.POINTER(_vp)),
     "rtcg_graph_launch": (_vp, _vp),
     "rtcg_graph_destroy": (_vp,),
+    "rtcg_ipc_get_handle": (_u64, ctypes.c_char_p),
+    "rtcg_ipc_open_handle": (ctypes.c_char_p, ctypes.POINTER(_u64)),
+    "rtcg_ipc_close_handle": (_u64,),
+    "rtcg_device_can_access_peer": (_int, _int, _pint),
 }
 
 EXPORTED_SYMBOLS = tuple(sorted(_PROTOTYPES)) + (
@@ -542,6 +546,34 @@ def memcpy_dtod(dst: int, src: int, nbytes: int, stream=None) -> None:
 def stream_synchronize(stream=None) -> None:
     s = current_stream() if stream is None else stream
     _check(lib().rtcg_stream_synchronize(s or None), "stream sync")
+
+
+def ipc_get_handle(dptr: int) -> bytes:
+    """64-byte CUDA IPC handle of an ``mem_alloc`` buffer."""
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().rtcg_ipc_get_handle(dptr, buf), "cuIpcGetMemHandle")
+    return buf.raw
+
+
+def ipc_open_handle(handle: bytes) -> int:
+    """Map another process's buffer into this context (peer access lazily
+    enabled); returns its device address here."""
+    if len(handle) != 64:
+        raise ValueError("an IPC handle is 64 bytes")
+    out = _u64()
+    _check(lib().rtcg_ipc_open_handle(handle, ctypes.byref(out)), "cuIpcOpenMemHandle")
+    return out.value
+
+
+def ipc_close_handle(dptr: int) -> None:
+    _check(lib().rtcg_ipc_close_handle(dptr), "cuIpcCloseMemHandle")
+
+
+def can_access_peer(device: int, peer: int) -> bool:
+    out = _int()
+    _check(lib().rtcg_device_can_access_peer(device, peer, ctypes.byref(out)),
+           "cuDeviceCanAccessPeer")
+    return bool(out.value)
 
 
 def host_alloc(nbytes: int) -> int:

@@ -112,6 +112,10 @@ struct Driver {
     X(cuGraphLaunch, CUresult(CUgraphExec, CUstream))                        \
     X(cuGraphExecDestroy, CUresult(CUgraphExec))                             \
     X(cuGraphDestroy, CUresult(CUgraph))                                     \
+    X(cuIpcGetMemHandle, CUresult(CUipcMemHandle *, CUdeviceptr))            \
+    X(cuIpcOpenMemHandle_v2, CUresult(CUdeviceptr *, CUipcMemHandle, unsigned)) \
+    X(cuIpcCloseMemHandle, CUresult(CUdeviceptr))                            \
+    X(cuDeviceCanAccessPeer, CUresult(int *, CUdevice, CUdevice))            \
     X(cuGetErrorString, CUresult(CUresult, const char **))
 #define RTCG_DECLARE(name, sig) fnptr<sig> name = nullptr;
     RTCG_DRIVER_FNS(RTCG_DECLARE)
@@ -934,3 +938,45 @@ int rtcg_graph_destroy(rtcg_graph_t graph) {
 }
 
 }  // extern "C"
+
+/* --- peer memory over NVLink / NVSwitch (CUDA IPC) ------------------------ */
+
+int rtcg_ipc_get_handle(uint64_t dptr, unsigned char handle[64]) {
+    NEED_CONTEXT();
+    if (!handle) return fail(RTCG_ERR_INVALID, "rtcg_ipc_get_handle: null handle");
+    CUipcMemHandle h;
+    CU_CALL(g_drv.cuIpcGetMemHandle(&h, dptr), "cuIpcGetMemHandle");
+    static_assert(sizeof(h.reserved) == 64, "CUipcMemHandle is 64 bytes");
+    memcpy(handle, h.reserved, 64);
+    return RTCG_OK;
+}
+
+int rtcg_ipc_open_handle(const unsigned char handle[64], uint64_t *dptr) {
+    NEED_CONTEXT();
+    if (!handle || !dptr) return fail(RTCG_ERR_INVALID, "rtcg_ipc_open_handle: null argument");
+    CUipcMemHandle h;
+    memcpy(h.reserved, handle, 64);
+    CUdeviceptr p = 0;
+    CU_CALL(g_drv.cuIpcOpenMemHandle_v2(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS),
+            "cuIpcOpenMemHandle");
+    *dptr = p;
+    return RTCG_OK;
+}
+
+int rtcg_ipc_close_handle(uint64_t dptr) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuIpcCloseMemHandle(dptr), "cuIpcCloseMemHandle");
+    return RTCG_OK;
+}
+
+int rtcg_device_can_access_peer(int device, int peer, int *can) {
+    int st = driver_ready();
+    if (st != RTCG_OK) return st;
+    if (!can) return fail(RTCG_ERR_INVALID, "rtcg_device_can_access_peer: null result");
+    CUdevice a, b;
+    CU_CALL(g_drv.cuDeviceGet(&a, device), "cuDeviceGet");
+    CU_CALL(g_drv.cuDeviceGet(&b, peer), "cuDeviceGet");
+    if (device == peer) { *can = 1; return RTCG_OK; }
+    CU_CALL(g_drv.cuDeviceCanAccessPeer(can, a, b), "cuDeviceCanAccessPeer");
+    return RTCG_OK;
+}

@@ -11,17 +11,25 @@ plumbing):
   local slice with ``base`` = the slice start, so ``i`` in user code stays the
   global index;
 * elementwise kernels need no communication;
-* reductions do one exchange over NCCL (NVLink / NVSwitch): an ncclAllReduce
-  of the 8-byte accumulators when the reduce_expr is exactly an NCCL op
-  (integer sum; max/min), otherwise an all-gather of the accumulators into a
-  world-sized buffer folded in ascending rank order by the kernel's compiled
-  ``<name>_combine`` -- valid for any ``reduce_expr`` and deterministic for a
-  fixed world size (float sums always take this path).
+* reductions do one exchange.  The product path (``collective="p2p"``) does
+  it inside the reduction kernel: its last CTA stores the device accumulator
+  into every rank's mailbox over NVLink / NVSwitch peer memory (CUDA IPC
+  mappings, :class:`PeerMailbox`), waits for the world's accumulators to land
+  in its own mailbox and folds them in ascending rank order -- one launch per
+  GPU, no collective call, any ``reduce_expr``, the same bits on every rank.
+  The NCCL paths remain as the baseline: an ncclAllReduce of the 8-byte
+  accumulators when the reduce_expr is exactly an NCCL op (integer sum;
+  max/min), otherwise an all-gather of the accumulators folded in rank order
+  by the kernel's compiled ``<name>_combine`` (same fold, same result).
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
+
+import ctypes
+import struct
+import threading
 
 import numpy as np
 
@@ -29,7 +37,8 @@ from . import _runtime
 from . import ndarray as nd
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
-           "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op"]
+           "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op", "PeerMailbox",
+           "peer_mailbox"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -141,19 +150,145 @@ def nccl_op(spec) -> str | None:
 _NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
 
 
+# --- peer-memory exchange (the fused cross-GPU combine) -------------------------------------
+
+XR_MAX = 64                             # rtcg::XR_MAX in templates/prelude.cuh
+MAILBOX_BYTES = 8 * (XR_MAX + 2 * XR_MAX)  # epoch flags + two accumulator banks
+_XR = struct.Struct(f"<ii{XR_MAX}Q")     # struct rtcg::xr {int rank, world; u64 mbox[64];}
+
+
+class PeerMailbox:
+    """Every rank's exchange mailbox, mapped into this process, plus the
+    device descriptor (``rtcg::xr``) a reduction kernel reads.
+
+    ``ReductionKernel.launch(..., peers=mailbox)`` turns the launch into a
+    cross-GPU reduction (``rtcg::exchange``).  Each call takes the next epoch;
+    all ranks must issue the same sequence of calls on a mailbox, one stream
+    at a time (calls on one mailbox are serialised by the stream).  Not
+    capturable in CUDA graphs (the epoch is a launch parameter)."""
+
+    def __init__(self, rank: int, world: int, addresses, *, owned=(), opened=()) -> None:
+        if not 1 <= world <= XR_MAX:
+            raise ValueError(f"world size must be in [1, {XR_MAX}], got {world}")
+        if len(addresses) != world or not 0 <= rank < world:
+            raise ValueError("need one mailbox address per rank")
+        self.rank, self.world = rank, world
+        self.addresses = tuple(int(a) for a in addresses)
+        self._owned, self._opened = list(owned), list(opened)
+        self._epoch = 0
+        self._lock = threading.Lock()
+        blob = _XR.pack(rank, world, *self.addresses, *([0] * (XR_MAX - world)))
+        self.descriptor = _runtime.mem_alloc(len(blob))
+        self._owned.append(self.descriptor)
+        host = ctypes.create_string_buffer(blob, len(blob))
+        _runtime.memcpy_htod(self.descriptor, ctypes.addressof(host), len(blob), 0)
+        _runtime.stream_synchronize(0)
+
+    def next_epoch(self) -> int:
+        with self._lock:
+            self._epoch += 1
+            return self._epoch
+
+    @staticmethod
+    def _new_box() -> int:
+        box = _runtime.mem_alloc(MAILBOX_BYTES)   # cuMemAlloc: IPC-exportable
+        _runtime.memset_async(box, 0, MAILBOX_BYTES, 0)
+        _runtime.stream_synchronize(0)
+        return box
+
+    @classmethod
+    def create(cls, group=None) -> "PeerMailbox":
+        """Collective over a torch.distributed group (one process per GPU):
+        allocate and zero this rank's mailbox, exchange CUDA IPC handles
+        (``all_gather_object``, which also orders every zeroing before any
+        use) and map the peers' mailboxes."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = cls._new_box()
+        mine = (_runtime.current_device(), _runtime.ipc_get_handle(box))
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        addresses, opened = [], []
+        for r, (_dev, handle) in enumerate(everyone):
+            if r == rank:
+                addresses.append(box)
+            else:
+                addr = _runtime.ipc_open_handle(handle)
+                addresses.append(addr)
+                opened.append(addr)
+        mb = cls(rank, world, addresses, owned=[box], opened=opened)
+        mb.devices = tuple(d for d, _ in everyone)
+        return mb
+
+    @classmethod
+    def local_group(cls, world: int) -> list["PeerMailbox"]:
+        """``world`` mailboxes on the current device, one per emulated rank
+        (single-process tests of the exchange protocol: launch rank r on its
+        own stream with ``peers=group[r]``)."""
+        boxes = [cls._new_box() for _ in range(world)]
+        group = [cls(r, world, boxes) for r in range(world)]
+        group[0]._owned.extend(boxes)
+        return group
+
+    def close(self) -> None:
+        for addr in self._opened:
+            _runtime.ipc_close_handle(addr)
+        for addr in self._owned:
+            _runtime.mem_free(addr)
+        self._opened, self._owned = [], []
+
+
+_mailboxes: dict = {}
+_mailbox_lock = threading.Lock()
+
+
+def peer_mailbox(group=None, stream: int = 0) -> PeerMailbox:
+    """The cached mailbox of (group, device, stream); created collectively on
+    first use (every rank must reach the first call together)."""
+    key = (id(group), _runtime.current_device(), stream)
+    with _mailbox_lock:
+        mb = _mailboxes.get(key)
+    if mb is None:
+        mb = PeerMailbox.create(group)
+        with _mailbox_lock:
+            _mailboxes[key] = mb
+    return mb
+
+
+def p2p_capable(group=None) -> bool:
+    """True when every rank runs on its own device and all pairs have peer
+    access (NVLink / NVSwitch on an HGX B200).  Ranks that share a device
+    (test setups) take the NCCL path under ``collective="auto"``."""
+    import torch.distributed as dist
+    key = ("capable", id(group))
+    hit = _mailboxes.get(key)
+    if hit is not None:
+        return hit
+    devices = [None] * dist.get_world_size(group)
+    dist.all_gather_object(devices, _runtime.current_device(), group=group)
+    ok = len(set(devices)) == len(devices) and all(
+        _runtime.can_access_peer(a, b) for a in devices for b in devices)
+    _mailboxes[key] = ok
+    return ok
+
+
 def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
                    collective: str = "auto"):
     """Global reduction of a ReductionKernel over sharded arguments.
 
-    1. local two-stage reduction into the kernel's scratch accumulator;
-    2. the cross-GPU step over NCCL (NVLink / NVSwitch):
-       ``"allreduce"`` -- one ncclAllReduce of the 8-byte accumulators when
-       :func:`nccl_op` maps ``reduce_expr`` to an exact NCCL op;
-       ``"allgather"`` -- all-gather (world x 8 bytes) + ``<name>_combine``
-       folding in rank order, valid for any ``reduce_expr``;
-       ``"auto"`` -- allreduce when exact, else allgather;
-    3. the out-dtype value is written on the device.
-    Everything runs in stream order on torch's current stream.
+    ``"p2p"`` -- one launch per GPU: the local two-stage reduction and the
+    exchange of accumulators over peer memory in the same kernel
+    (:class:`PeerMailbox`), folded in rank order; any ``reduce_expr``.
+
+    NCCL baseline -- the local reduction, then:
+    ``"allreduce"`` -- one ncclAllReduce of the 8-byte accumulators when
+    :func:`nccl_op` maps ``reduce_expr`` to an exact NCCL op;
+    ``"allgather"`` -- all-gather (world x 8 bytes) + ``<name>_combine``
+    folding in rank order, valid for any ``reduce_expr``.
+
+    ``"auto"`` -- p2p when every rank has its own peer-accessible GPU, else
+    allreduce when exact, else allgather.  Everything runs in stream order on
+    torch's current stream; p2p and allgather give identical bits.
     """
     import torch
     import torch.distributed as dist
@@ -163,12 +298,24 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
     spec = kernel.spec
     op = nccl_op(spec)
     if collective == "auto":
-        collective = "allreduce" if op is not None else "allgather"
+        collective = "p2p" if p2p_capable(group) else \
+            "allreduce" if op is not None else "allgather"
     if collective == "allreduce" and op is None:
         raise ValueError(f"reduce_expr {spec.reduce_expr!r} has no exact NCCL equivalent")
-    if collective not in ("allreduce", "allgather"):
+    if collective not in ("allreduce", "allgather", "p2p"):
         raise ValueError(f"unknown collective {collective!r}")
     stream = torch.cuda.current_stream().cuda_stream
+    if collective == "p2p":
+        mailbox = peer_mailbox(group, stream)
+        with _runtime.use_stream(stream):
+            first = next(a for a in local_args if isinstance(a, nd.NdArray))
+            out = first.pool.alloc_uninitialized(spec.out_dtype, ())
+            kernel.launch(*local_args, n=n_local, base=base, out=out, peers=mailbox)
+            if return_device:
+                return out
+            value = out.to_host()
+            out.free()
+            return spec.out_dtype.np.type(value[()])
     with _runtime.use_stream(stream):
         scratch = kernel.launch(*local_args, n=n_local, base=base)
         acc_view = torch.as_tensor(_DeviceView(scratch.result, 1, spec.acc_dtype), device="cuda")

@@ -208,7 +208,7 @@ class ReductionKernel:
             self.smem, self._tma_tile = tp["tma_smem"], tp["tile"]
         self.combine = jit.get_kernel(self.module, f"{name}_combine")
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
-        self._binder = cg.Binder(sig, extra=4)
+        self._binder = cg.Binder(sig, extra=6)
         self._waves = 1 if self.variant.waves is None else self.variant.waves
         self._scratch: dict[int, _Scratch] = {}
         self._lock = threading.Lock()
@@ -276,28 +276,42 @@ class ReductionKernel:
                     f"{self.spec.reduce_expr!r}: fold([{value!r}]) gave {folded!r}")
 
     def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
-               out: nd.NdArray | None = None):
+               out: nd.NdArray | None = None, peers=None):
         """Asynchronous stage 1+2.  Returns the scratch (result address holds
         the accumulator, ``out`` -- or the scratch out slot -- the out-dtype
-        value).  Used by ``__call__`` and by the multi-GPU driver."""
+        value).  Used by ``__call__`` and by the multi-GPU driver.
+
+        ``peers`` (a :class:`~paper_0911_3456_b200.parallel.PeerMailbox`)
+        makes the launch a cross-GPU reduction: the kernel's last CTA
+        exchanges the device accumulator with every rank over peer memory and
+        result/out receive the global value (every rank must make the same
+        call; an empty local span still takes part)."""
         if n is not None and n < 0:
             raise nd.ShapeMismatch(f"n must be non-negative, got {n}")
         vals, ptrs, vectors, n = self._binder.bind(args, n, base, self.name, _ERRORS)
         dev = _runtime.current_device()
         s = self.scratch(dev, stream)
         out_addr = out.address if out is not None else s.out
-        if n == 0:
+        b = self._binder
+        if peers is not None:
+            vals[b.count + 6], vals[b.count + 7] = peers.descriptor, peers.next_epoch()
+        else:
+            vals[b.count + 6] = vals[b.count + 7] = 0
+        if n == 0 and peers is None:
             s.ensure(1)
             self._launch_combine(s.partials, 0, s.result, out_addr, stream)
             return s
-        handle, per_thread, smem = self._pick(vectors, n)
-        fn = handle.function(dev)
-        if smem:
-            _runtime.set_max_dynamic_smem(fn, smem)
-        grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
-                           self._waves, smem)
+        if n == 0:
+            handle, grid, smem = self.generic, 1, 0
+            fn = handle.function(dev)
+        else:
+            handle, per_thread, smem = self._pick(vectors, n)
+            fn = handle.function(dev)
+            if smem:
+                _runtime.set_max_dynamic_smem(fn, smem)
+            grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
+                               self._waves, smem)
         s.ensure(grid)
-        b = self._binder
         b.set_range(vals, base, base + n)
         vals[b.count + 2] = s.partials
         vals[b.count + 3] = s.result

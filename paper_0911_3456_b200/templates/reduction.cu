@@ -25,7 +25,7 @@ __device__ __forceinline__ auto rtcg_map(const long i${map_params})
 extern "C" __global__ void __launch_bounds__(${block})
 ${name}_g(${kparams_generic}, const long start, const long end,
     ${acc_t} *rtcg_partials, ${acc_t} *rtcg_result, ${out_t} *rtcg_out,
-    unsigned int *rtcg_ticket)
+    unsigned int *rtcg_ticket, const rtcg::xr *rtcg_xr, const unsigned long long rtcg_epoch)
 {
 ${unpack}
     ${acc_t} acc = ${neutral};
@@ -34,7 +34,7 @@ ${unpack}
         acc = rtcg_fold(acc, rtcg_map<${ptr_types_generic}>(i${call_args}));
     });
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
 }
 {% if tma %}
 // TMA path: a producer warp streams ${stages} ring stages of ${tile}-element
@@ -46,7 +46,8 @@ ${unpack}
 extern "C" __global__ void __launch_bounds__(${block})
 ${name}(${kparams_vector}, const long start, const long end,
     ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
-    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket)
+    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
+    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
 {
 ${unpack}
     constexpr int E = ${width};
@@ -112,7 +113,7 @@ ${smem_loads}
         }
     }
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
 }
 {% endif %}
 {% if vector %}
@@ -121,7 +122,8 @@ ${smem_loads}
 extern "C" __global__ void __launch_bounds__(${block})
 ${name}(${kparams_vector}, const long start, const long end,
     ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
-    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket)
+    ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
+    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
 {
 ${unpack}
     constexpr int E = ${width};
@@ -154,7 +156,7 @@ ${vec_loads}
         }
     }
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
 }
 {% endif %}
 // Ordered fold of partials[start, end) from the neutral into result[0]; the

@@ -268,3 +268,16 @@ def test_template_locals_never_clash_with_user_names(nvrtc_cache, cache):
     spec = rd.ReductionSpec("float *b, long G, float *t", nd.float64, "0", "a + b",
                             "b[i] * t[i] + G")
     jit.compile(rd.generate_reduction_source(spec, "clash_r", v), cache=nvrtc_cache)
+
+
+def test_peer_descriptor_layout_matches_prelude(nvrtc_cache):
+    """parallel.PeerMailbox packs rtcg::xr on the host; the device struct must
+    agree (size -- 8 + 8 * XR_MAX leaves no room for padding before mbox --,
+    slot count, mailbox size)."""
+    from paper_0911_3456_b200 import parallel as par
+    src = (cg.template("prelude.cuh")
+           + f"\nstatic_assert(sizeof(rtcg::xr) == {par._XR.size}, \"xr size\");"
+           + f"\nstatic_assert(rtcg::XR_MAX == {par.XR_MAX}, \"XR_MAX\");"
+           + '\nextern "C" __global__ void layout_probe() {}\n')
+    jit.compile(src, cache=nvrtc_cache)
+    assert par.MAILBOX_BYTES == 8 * 3 * par.XR_MAX
