@@ -134,7 +134,7 @@ class Dist:
             print(f"warning: --gpus {gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
         self.torch = None
         # RTCG_BENCH_FORCE_DIST=1 runs the multi-GPU code path (process group,
-        # NCCL all-gather of partials) even at world size 1
+        # cross-GPU exchange of the accumulators) even at world size 1
         self.forced = os.environ.get("RTCG_BENCH_FORCE_DIST") == "1"
         if self.world > 1 or self.forced:
             if "MASTER_ADDR" not in os.environ:
@@ -285,12 +285,20 @@ def run_ours(args) -> int:
         kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
         out = pool.alloc_uninitialized(nd.float32, ())
 
+        collective = None
         if not d.distributed:
             def step():
                 kernel.launch(gx, gy, out=out)
         else:
+            # the product path: one launch per GPU, accumulators exchanged over
+            # NVLink peer memory inside the kernel; NCCL only when peers are
+            # unreachable (RTCG_BENCH_COLLECTIVE overrides, e.g. "allgather")
+            collective = os.environ.get("RTCG_BENCH_COLLECTIVE") or (
+                "p2p" if par.p2p_capable() else "auto")
+
             def step():
-                par.sharded_reduce(kernel, sx, sy, return_device=True).free()
+                par.sharded_reduce(kernel, sx, sy, return_device=True,
+                                   collective=collective).free()
 
         # correctness of the tuned kernel on this data (cheap, before timing)
         value = kernel(gx, gy)
@@ -304,7 +312,9 @@ def run_ours(args) -> int:
         launches0 = kernel.launches
         with ClockSampler(d.local) as clocks:
             total_ms, per_step = _time_steps(rt, step, args.steps)
-        launches = kernel.launches - launches0 + (args.steps if d.distributed else 0)
+        # NCCL paths add one combine launch per step; p2p is one kernel
+        launches = kernel.launches - launches0 + (
+            args.steps if d.distributed and collective != "p2p" else 0)
         rt.synchronize()
         d.barrier()
         step_ms = d.max(total_ms / args.steps)
@@ -350,7 +360,8 @@ def run_ours(args) -> int:
                    "variant": best, "autotune_seconds": round(tune_s, 2),
                    "autotune_from_store": tuned.from_store,
                    "l2": "inputs 2 GiB per GPU > 126 MB L2 (no flush needed)",
-                   "parallelism": f"shards{d.world}" + ("+nccl" if d.distributed else ""),
+                   "parallelism": f"shards{d.world}" + (f"+{collective}" if d.distributed
+                                                        else ""),
                    "accumulator": "float64",
                    "gpu": info["name"], "result_finite": terms_ok},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,

@@ -449,6 +449,17 @@ int rtcg_module_function(rtcg_module_t module, const char *name, rtcg_function_t
     CUresult r = g_drv.cuModuleGetFunction(&f, reinterpret_cast<CUmodule>(module), name);
     if (r == CUDA_ERROR_NOT_FOUND) return fail(RTCG_ERR_NOT_FOUND, "kernel symbol '%s' not found", name);
     if (r != CUDA_SUCCESS) return cu_fail(r, "cuModuleGetFunction");
+    // Load the kernel's code now rather than at its first launch (CUDA's lazy
+    // loading): a load may wait for running kernels, which must not happen
+    // between the launches of kernels that wait on each other (the peer
+    // exchange of multi-GPU reductions).  cuFuncLoad is optional (CUDA 12.4+).
+    using func_load_t = CUresult (*)(CUfunction);
+    static func_load_t func_load =
+        reinterpret_cast<func_load_t>(dlsym(g_drv.handle, "cuFuncLoad"));
+    if (func_load) {
+        r = func_load(f);
+        if (r != CUDA_SUCCESS) return cu_fail(r, "cuFuncLoad");
+    }
     *function = reinterpret_cast<rtcg_function_t>(f);
     return RTCG_OK;
 }

@@ -294,6 +294,11 @@ class ReductionKernel:
         out_addr = out.address if out is not None else s.out
         b = self._binder
         if peers is not None:
+            # resolve (and load) every entry point before the first exchange
+            # launch: nothing may wait on the device between ranks' launches
+            for h in (self.generic, self.vectorized, self.combine):
+                if h is not None:
+                    h.function(dev)
             vals[b.count + 6], vals[b.count + 7] = peers.descriptor, peers.next_epoch()
         else:
             vals[b.count + 6] = vals[b.count + 7] = 0
