@@ -1,6 +1,8 @@
 """Build the native runtime in tree: ``python -m paper_0911_3456_b200._build``.
 
 * ``librtcg_b200.so`` -- the C-ABI runtime (NVRTC + CUDA driver; host code).
+* ``_fastlaunch*.so`` -- CPython extension: per-call argument marshalling,
+  vector-path / grid decisions and the launch of generated kernels in C++.
 * ``prebuilt/*.cubin`` -- ahead-of-time nvcc builds of the kernel templates
   instantiated for the stock kernels (axpy, dot, sum, max|x|), compiled with
   ``-gencode arch=compute_100a,code=sm_100a -lineinfo``.  They prove the
@@ -52,6 +54,19 @@ def build_runtime(force: bool = False) -> Path:
     return LIB
 
 
+def build_fastlaunch(force: bool = False) -> Path:
+    import sysconfig
+    src = CSRC / "fastlaunch.cpp"
+    target = PKG / f"_fastlaunch{sysconfig.get_config_var('EXT_SUFFIX')}"
+    if force or _stale(target, src):
+        cxx = os.environ.get("CXX") or shutil.which("g++") or "c++"
+        tmp = target.with_suffix(".tmp")
+        _run([cxx, "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall",
+              f"-I{sysconfig.get_paths()['include']}", str(src), "-o", str(tmp)])
+        os.replace(tmp, target)
+    return target
+
+
 def build_prebuilt(force: bool = False) -> list[Path]:
     """nvcc-compile the stock kernel instantiations to sm_100a cubins."""
     from . import aot  # generates the stock kernel sources
@@ -76,6 +91,7 @@ def main(argv=None) -> int:
     argv = list(sys.argv[1:] if argv is None else argv)
     force = "--force" in argv
     print(build_runtime(force))
+    print(build_fastlaunch(force))
     if "--no-prebuilt" not in argv:
         for p in build_prebuilt(force):
             print(p)

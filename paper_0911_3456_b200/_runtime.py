@@ -195,6 +195,25 @@ def lib() -> ctypes.CDLL:
         return _lib
 
 
+_fast = None
+
+
+def fastlaunch():
+    """The native launch-path extension (``_fastlaunch``), wired to this
+    library's ``rtcg_launch``.  Built with the runtime; missing = not built."""
+    global _fast
+    if _fast is None:
+        try:
+            from . import _fastlaunch as mod
+        except ImportError as exc:
+            raise RuntimeMissing(
+                f"_fastlaunch is not built ({exc}); run `python -m paper_0911_3456_b200._build`"
+            ) from exc
+        mod.set_launcher(ctypes.cast(lib().rtcg_launch, ctypes.c_void_p).value)
+        _fast = mod
+    return _fast
+
+
 def _check(status: int, what: str = "") -> None:
     if status == RTCG_OK:
         return

@@ -211,6 +211,7 @@ class ReductionKernel:
         self._binder = cg.Binder(sig, extra=6)
         self._waves = 1 if self.variant.waves is None else self.variant.waves
         self._scratch: dict[int, _Scratch] = {}
+        self._plans: dict = {}
         self._lock = threading.Lock()
         self.launches = 0
         if debug:
@@ -275,6 +276,36 @@ class ReductionKernel:
                     f"neutral {self.spec.neutral!r} is not an identity for "
                     f"{self.spec.reduce_expr!r}: fold([{value!r}]) gave {folded!r}")
 
+    def _plan(self, dev: int):
+        """Native launch plan on device *dev* (``csrc/fastlaunch.cpp``): the
+        binder, :meth:`_pick` and the grid policy in one C call."""
+        plan = self._plans.get(dev)
+        if plan is not None:
+            return plan
+        sms = cg.sm_count(dev)
+        block = self.variant.block
+        gen_fn = self.generic.function(dev)
+        gen = (gen_fn, self.variant.unroll, sms * max(1, _runtime.occupancy(gen_fn, block, 0)),
+               self._waves, 0)
+        vec = None
+        if self.vectorized is not None:
+            fn = self.vectorized.function(dev)
+            if self.smem:
+                _runtime.set_max_dynamic_smem(fn, self.smem)
+                per = max(1, self._tma_tile // block)
+            else:
+                per = self.variant.unroll * self.width
+            vec = (fn, per, sms * max(1, _runtime.occupancy(fn, block, self.smem)), self._waves,
+                   self.smem)
+        params = []
+        for p in self.spec.signature.params:
+            acc = self.access[p.name] if self.access is not None and p.is_vector else None
+            params.append((p.is_vector, p.dtype, p.dtype.size, p.dtype.kind,
+                           bool(acc and acc.used), bool(acc and acc.written)))
+        plan = self._plans[dev] = _runtime.fastlaunch().Plan(
+            params, nd.NdArray, block, self.variant.workers or 0, gen, vec, 6)
+        return plan
+
     def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
                out: nd.NdArray | None = None, peers=None):
         """Asynchronous stage 1+2.  Returns the scratch (result address holds
@@ -286,6 +317,24 @@ class ReductionKernel:
         exchanges the device accumulator with every rank over peer memory and
         result/out receive the global value (every rank must make the same
         call; an empty local span still takes part)."""
+        if peers is None:
+            tls = _runtime._tls
+            dev = getattr(tls, "device", None)
+            if dev is None:
+                dev = _runtime.current_device()
+            st = getattr(tls, "stream", 0) if stream is None else stream
+            s = self._scratch.get((dev, st)) or self.scratch(dev, st)
+            plan = self._plans.get(dev) or self._plan(dev)
+            got = plan.launch(args, n, base, st or 0, s.capacity,
+                              (s.partials, s.result, s.out if out is None else out.address,
+                               s.ticket, 0, 0))
+            if got:          # None: the Python binder below; 0: empty span
+                if got < 0:
+                    _runtime._check(-got, "launch")
+                self.launches += 1
+                return s
+        # the Python binder: empty spans, peer exchanges, and every call the
+        # native plan declined (it raises the reference's exceptions)
         if n is not None and n < 0:
             raise nd.ShapeMismatch(f"n must be non-negative, got {n}")
         vals, ptrs, vectors, n = self._binder.bind(args, n, base, self.name, _ERRORS)

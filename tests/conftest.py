@@ -19,6 +19,7 @@ def pytest_configure(config):
 def _ensure_runtime():
     from paper_0911_3456_b200 import _build
     _build.build_runtime()
+    _build.build_fastlaunch()
 
 
 _ensure_runtime()
