@@ -208,14 +208,26 @@ class PeerMailbox:
         mine = (_runtime.current_device(), _runtime.ipc_get_handle(box))
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
-        addresses, opened = [], []
-        for r, (_dev, handle) in enumerate(everyone):
-            if r == rank:
-                addresses.append(box)
-            else:
-                addr = _runtime.ipc_open_handle(handle)
-                addresses.append(addr)
-                opened.append(addr)
+        addresses, opened, error = [], [], None
+        try:
+            for r, (_dev, handle) in enumerate(everyone):
+                if r == rank:
+                    addresses.append(box)
+                else:
+                    addr = _runtime.ipc_open_handle(handle)
+                    addresses.append(addr)
+                    opened.append(addr)
+        except Exception as exc:  # noqa: BLE001 - decided collectively below
+            error = exc
+        # every rank must take the exchange path or none: agree on success
+        verdicts = [None] * world
+        dist.all_gather_object(verdicts, error is None, group=group)
+        if not all(verdicts):
+            for addr in opened:
+                _runtime.ipc_close_handle(addr)
+            _runtime.mem_free(box)
+            raise RuntimeError(f"peer mailboxes unavailable on ranks "
+                               f"{[r for r, ok in enumerate(verdicts) if not ok]}: {error}")
         mb = cls(rank, world, addresses, owned=[box], opened=opened)
         mb.devices = tuple(d for d, _ in everyone)
         return mb
