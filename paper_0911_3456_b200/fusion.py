@@ -34,48 +34,30 @@ _SYMBOLS = {"add": "+", "sub": "-", "mul": "*", "div": "/"}
 
 
 class Expr:
-    """A traced elementwise expression over GPUArrays and scalars."""
+    """A traced elementwise expression over GPUArrays and scalars.
 
-    __slots__ = ("text", "dtype", "arrays", "scalars", "shape")
+    The trace is a small tuple tree -- ``("A", array)`` leaves, ``("S", value,
+    dtype)`` scalar leaves, ``(symbol, cname, left, right)`` operators --
+    built with no string work; the C text is rendered only when a new kernel
+    must be generated (the per-call cost of a fused chain is the trace, one
+    tree walk and the native launch)."""
 
-    def __init__(self, text: str, dtype: nd.Dtype, arrays: tuple, scalars: tuple, shape):
-        self.text, self.dtype, self.arrays, self.scalars, self.shape = \
-            text, dtype, arrays, scalars, shape
+    __slots__ = ("node", "dtype", "shape")
+
+    def __init__(self, node: tuple, dtype: nd.Dtype, shape) -> None:
+        self.node, self.dtype, self.shape = node, dtype, shape
 
     # -- building ------------------------------------------------------------------------
 
-    def _merge(self, other: "Expr"):
-        """Union of leaves; returns (arrays, scalars, remap of other's names)."""
-        arrays, scalars = list(self.arrays), list(self.scalars)
-        text = other.text
-        ids = {id(a): k for k, a in enumerate(arrays)}
-        renames = {}
-        for k, a in enumerate(other.arrays):
-            j = ids.get(id(a))
-            if j is None:
-                j = len(arrays)
-                arrays.append(a)
-                ids[id(a)] = j
-            renames[f"rtcg_fa{k}"] = f"rtcg_fa{j}"
-        for k, s in enumerate(other.scalars):
-            renames[f"rtcg_fs{k}"] = f"rtcg_fs{len(scalars)}"
-            scalars.append(s)
-        if renames:
-            import re
-            text = re.sub(r"\brtcg_f[as]\d+\b", lambda m: renames.get(m.group(0), m.group(0)),
-                          text)
-        return tuple(arrays), tuple(scalars), text
-
     def _binop(self, other, op: str, reverse: bool) -> "Expr":
         symbol = _SYMBOLS[op]
-        if isinstance(other, NdArray):
+        if other.__class__ is NdArray or isinstance(other, NdArray):
             other = lazy(other)
         if isinstance(other, Expr):
             if other.shape != self.shape:
                 raise ShapeMismatch(f"operand shapes differ: {self.shape} vs {other.shape}")
-            arrays, scalars, other_text = self._merge(other)
             rt = nd.promote(self.dtype, other.dtype)
-            left, right = (other_text, self.text) if reverse else (self.text, other_text)
+            right = other.node
         else:
             sd = ew._scalar_dtype_of(other)
             if sd is nd.int64 and not isinstance(other, np.generic):
@@ -83,13 +65,9 @@ class Expr:
             rt = nd.promote(self.dtype, sd)
             if op == "div" and rt.kind != "f" and not reverse and int(other) == 0:
                 raise DivisionByZero("integer division by scalar zero")
-            arrays = self.arrays
-            scalars = self.scalars + ((other, sd),)
-            name = f"rtcg_fs{len(self.scalars)}"
-            left, right = (name, self.text) if reverse else (self.text, name)
-        c = rt.cname
-        text = f"(({c}) (({c}) {left} {symbol} ({c}) {right}))"
-        return Expr(text, rt, arrays, scalars, self.shape)
+            right = ("S", other, sd)
+        left, right = (right, self.node) if reverse else (self.node, right)
+        return Expr((symbol, rt.cname, left, right), rt, self.shape)
 
     def __add__(self, o): return self._binop(o, "add", False)
     def __radd__(self, o): return self._binop(o, "add", True)
@@ -100,15 +78,60 @@ class Expr:
     def __truediv__(self, o): return self._binop(o, "div", False)
     def __rtruediv__(self, o): return self._binop(o, "div", True)
 
+    # -- views of the trace ----------------------------------------------------------------
+
+    def _leaves(self):
+        """(structure key, arrays in first-use order, scalars as (value, dtype))."""
+        arrays, ids, scalars = [], {}, []
+
+        def walk(n):
+            tag = n[0]
+            if tag == "A":
+                a = n[1]
+                k = ids.get(id(a))
+                if k is None:
+                    k = ids[id(a)] = len(arrays)
+                    arrays.append(a)
+                return ("a", k, a.dtype.name)
+            if tag == "S":
+                scalars.append((n[1], n[2]))
+                return ("s", len(scalars) - 1, n[2].name)
+            return (tag, n[1], walk(n[2]), walk(n[3]))
+        return walk(self.node), tuple(arrays), tuple(scalars)
+
+    @property
+    def arrays(self) -> tuple:
+        return self._leaves()[1]
+
+    @property
+    def scalars(self) -> tuple:
+        return self._leaves()[2]
+
+    @property
+    def text(self) -> str:
+        """The C expression, leaves named ``rtcg_fa<k>`` / ``rtcg_fs<k>``."""
+        return _render(self._leaves()[0], "")
+
     def __repr__(self) -> str:
         return f"<Expr {self.dtype.name} {self.text}>"
+
+
+def _render(key, index: str) -> str:
+    tag = key[0]
+    if tag == "a":
+        return f"rtcg_fa{key[1]}{index}"
+    if tag == "s":
+        return f"rtcg_fs{key[1]}"
+    c = key[1]
+    return (f"(({c}) (({c}) {_render(key[2], index)} {tag} "
+            f"({c}) {_render(key[3], index)}))")
 
 
 def lazy(array: NdArray) -> Expr:
     """A leaf expression reading *array*."""
     if not isinstance(array, NdArray):
         raise TypeError("lazy() takes a GPUArray")
-    return Expr("rtcg_fa0", array.dtype, (array,), (), array.shape)
+    return Expr(("A", array), array.dtype, array.shape)
 
 
 _memo: dict = {}
@@ -121,28 +144,26 @@ def kernel_count() -> int:
         return len(_memo)
 
 
-def _kernel(expr: Expr, out_dtype: nd.Dtype) -> ew.ElementwiseKernel:
-    params = [ew.KernelParam(f"rtcg_fa{k}", a.dtype, True) for k, a in enumerate(expr.arrays)]
-    params += [ew.KernelParam(f"rtcg_fs{k}", sd, False) for k, (_, sd) in enumerate(expr.scalars)]
-    params.append(ew.KernelParam("rtcg_fo", out_dtype, True))
-    key = (expr.text, tuple((p.name, p.dtype.name, p.is_vector) for p in params))
-    with _memo_lock:
-        kernel = _memo.get(key)
+def _kernel_for(key, arrays, scalars, out_dtype: nd.Dtype) -> ew.ElementwiseKernel:
+    memo_key = (key, out_dtype.name)
+    kernel = _memo.get(memo_key)
     if kernel is None:
         import hashlib
+        params = [ew.KernelParam(f"rtcg_fa{k}", a.dtype, True) for k, a in enumerate(arrays)]
+        params += [ew.KernelParam(f"rtcg_fs{k}", sd, False) for k, (_, sd) in enumerate(scalars)]
+        params.append(ew.KernelParam("rtcg_fo", out_dtype, True))
         sig = ew.KernelSignature(tuple(params))
-        op = "rtcg_fo[i] = " + _index(expr.text) + ";"
-        tag = hashlib.sha256(repr(key).encode()).hexdigest()[:12]
+        op = "rtcg_fo[i] = " + _render(key, "[i]") + ";"
+        tag = hashlib.sha256(repr(memo_key).encode()).hexdigest()[:12]
         kernel = ew.ElementwiseKernel(sig, op, f"fused_{tag}")
         with _memo_lock:
-            kernel = _memo.setdefault(key, kernel)
+            kernel = _memo.setdefault(memo_key, kernel)
     return kernel
 
 
-def _index(text: str) -> str:
-    """Leaf names -> element references (``rtcg_fa0`` -> ``rtcg_fa0[i]``)."""
-    import re
-    return re.sub(r"\b(rtcg_fa\d+)\b", r"\1[i]", text)
+def _kernel(expr: Expr, out_dtype: nd.Dtype) -> ew.ElementwiseKernel:
+    key, arrays, scalars = expr._leaves()
+    return _kernel_for(key, arrays, scalars, out_dtype)
 
 
 def evaluate(expr, out: NdArray | None = None, stream=None) -> NdArray:
@@ -151,13 +172,13 @@ def evaluate(expr, out: NdArray | None = None, stream=None) -> NdArray:
         return expr
     if not isinstance(expr, Expr):
         raise TypeError("evaluate() takes an Expr")
-    first = expr.arrays[0]
+    key, arrays, scalars = expr._leaves()
     if out is None:
-        out = first.pool.alloc_uninitialized(expr.dtype, expr.shape)
+        out = arrays[0].pool.alloc_uninitialized(expr.dtype, expr.shape)
     elif out.dtype != expr.dtype or out.shape != expr.shape:
         raise ShapeMismatch("out does not match the expression's dtype/shape")
-    kernel = _kernel(expr, expr.dtype)
-    kernel(*expr.arrays, *(v for v, _ in expr.scalars), out, n=out.size, stream=stream)
+    kernel = _kernel_for(key, arrays, scalars, expr.dtype)
+    kernel(*arrays, *[v for v, _ in scalars], out, n=out.size, stream=stream)
     return out
 
 
@@ -165,7 +186,8 @@ def fused(fn):
     """Decorator: ``fused(f)(*arrays)`` traces ``f`` over lazy leaves and
     evaluates it as one kernel."""
     def run(*args, out=None, stream=None):
-        traced = fn(*(lazy(a) if isinstance(a, NdArray) else a for a in args))
+        traced = fn(*(Expr(("A", a), a.dtype, a.shape) if a.__class__ is NdArray else
+                      lazy(a) if isinstance(a, NdArray) else a for a in args))
         return evaluate(traced, out=out, stream=stream)
     run.__name__ = getattr(fn, "__name__", "fused")
     return run
