@@ -186,3 +186,37 @@ def test_two_processes_exchange_through_ipc_mailboxes(tmp_path):
     n = 2_000_003
     host = np.random.default_rng(13).integers(-(1 << 40), 1 << 40, n, dtype=np.int64)
     assert results[0] == results[1] == [int(host.sum())] * 3
+
+
+def test_emulated_ranks_survive_skew_over_many_epochs(pool):
+    """Random per-rank delays before each reduction (a busy kernel of random
+    length on the rank's stream) make ranks run ahead into the next epoch
+    while others still fold: every rank must still get the exact ordered
+    fold, round after round (parity banks + monotone epochs)."""
+    from paper_0911_3456_b200 import _runtime as rt, elementwise as ew, ndarray as nd
+    from paper_0911_3456_b200 import reduction as rd
+    world, rounds = 4, 60
+    rng = np.random.default_rng(21)
+    x = rng.integers(-1000, 1000, 200_003).astype(np.int64)
+    shards = _shard(pool, nd.int64, [x], world)
+    k = rd.sum_kernel(nd.int64)
+    want = int(x.sum())
+    spin = ew.ElementwiseKernel("long iters, float *w",
+                                "float a = w[i]; for (long t = 0; t < iters; ++t) "
+                                "a = a * 0.999f + 0.001f; w[i] = a", "spin")
+    busy = [pool.alloc(nd.float32, (4096,)) for _ in range(world)]
+    group = par.PeerMailbox.local_group(world)
+    streams = [rt.Stream() for _ in range(world)]
+    outs = [[pool.alloc_uninitialized(nd.int64, ()) for _ in range(world)] for _ in range(rounds)]
+    for j in range(rounds):
+        for r in rng.permutation(world):
+            with rt.use_stream(streams[r].handle):
+                spin(int(rng.integers(0, 20000)), busy[r])
+                s = k.launch(*shards[r][0], base=shards[r][1], peers=group[r])
+                rt.memcpy_dtod(outs[j][r].address, s.result, 8)
+    for st in streams:
+        st.synchronize()
+    got = [[int(o.get()[()]) for o in row] for row in outs]
+    assert got == [[want] * world] * rounds
+    for m in group:
+        m.close()
