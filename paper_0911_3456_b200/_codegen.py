@@ -42,6 +42,9 @@ CACHE_POLICIES = {
     "default": (1, 0, 0),
     "streaming": (2, 2, 1),
     "no-l1": (3, 0, 2),
+    # read-only loads ask L2 for the whole 256-byte block (ld...L2::256B)
+    "l2-256": (4, 0, 0),
+    "l2-256-no-l1": (5, 0, 2),
     # inputs staged through shared memory by TMA bulk copies (the "TMA path"
     # of templates/reduction.cu and templates/elementwise.cu); the policies
     # apply to the pointer-path head/tail and to elementwise stores
