@@ -231,8 +231,19 @@ def run_reference(args) -> int:
 # --- GPU arm ----------------------------------------------------------------------------------------
 
 
-def _time_steps(rt, step, k: int):
-    """Device time of k steps on the current stream, plus per-step durations."""
+def _time_steps(rt, step, k: int, per_step: bool = True):
+    """Device time of k steps on the current stream, plus per-step durations
+    (``per_step=False``: only the two bracketing events, so nothing is
+    recorded between back-to-back launches; per-step = the mean)."""
+    if not per_step:
+        start, stop = rt.Event(), rt.Event()
+        start.record()
+        for _ in range(k):
+            step()
+        stop.record()
+        stop.synchronize()
+        total = start.elapsed_ms(stop)
+        return total, [total / k] * k
     events = [rt.Event() for _ in range(k + 1)]
     events[0].record()
     for j in range(k):
@@ -293,6 +304,8 @@ def run_ours(args) -> int:
             run()
             confirm.append((min(run() for _ in range(2)), e.as_dict()))
         best = min(confirm, key=lambda c: c[0])[1] if confirm else tuned.best_assignment
+        if os.environ.get("RTCG_BENCH_DOT_VARIANT"):   # experiments: pin the variant
+            best = json.loads(os.environ["RTCG_BENCH_DOT_VARIANT"])
         tune_s = time.perf_counter() - t0
         kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
 
@@ -330,7 +343,8 @@ def run_ours(args) -> int:
         rt.synchronize()
         launches0 = kernel.launches
         with ClockSampler(d.local) as clocks:
-            total_ms, per_step = _time_steps(rt, step, args.steps)
+            total_ms, per_step = _time_steps(rt, step, args.steps,
+                                             os.environ.get("RTCG_BENCH_STEP_EVENTS", "0") == "1")
         # NCCL paths add one combine launch per step; p2p is one kernel
         launches = kernel.launches - launches0 + (
             args.steps if d.distributed and collective != "p2p" else 0)
