@@ -250,20 +250,31 @@ class PeerMailbox:
         self._opened, self._owned = [], []
 
 
+# Per-process caches keyed by the identity of the process-group object (the
+# entry holds the object, so a destroyed-and-recreated group -- possibly of
+# another size, possibly reusing the address -- never matches a stale entry).
 _mailboxes: dict = {}
+_capable: dict = {}
 _mailbox_lock = threading.Lock()
+
+
+def _group_object(group):
+    import torch.distributed as dist
+    return group if group is not None else dist.group.WORLD
 
 
 def peer_mailbox(group=None, stream: int = 0) -> PeerMailbox:
     """The cached mailbox of (group, device, stream); created collectively on
     first use (every rank must reach the first call together)."""
-    key = (id(group), _runtime.current_device(), stream)
+    g = _group_object(group)
+    key = (_runtime.current_device(), stream)
     with _mailbox_lock:
-        mb = _mailboxes.get(key)
-    if mb is None:
-        mb = PeerMailbox.create(group)
-        with _mailbox_lock:
-            _mailboxes[key] = mb
+        for owner, mb in _mailboxes.get(key, ()):
+            if owner is g:
+                return mb
+    mb = PeerMailbox.create(group)
+    with _mailbox_lock:
+        _mailboxes.setdefault(key, []).append((g, mb))
     return mb
 
 
@@ -272,15 +283,15 @@ def p2p_capable(group=None) -> bool:
     access (NVLink / NVSwitch on an HGX B200).  Ranks that share a device
     (test setups) take the NCCL path under ``collective="auto"``."""
     import torch.distributed as dist
-    key = ("capable", id(group))
-    hit = _mailboxes.get(key)
-    if hit is not None:
-        return hit
+    g = _group_object(group)
+    for owner, ok in _capable.get(id(g), ()):
+        if owner is g:
+            return ok
     devices = [None] * dist.get_world_size(group)
     dist.all_gather_object(devices, _runtime.current_device(), group=group)
     ok = len(set(devices)) == len(devices) and all(
         _runtime.can_access_peer(a, b) for a in devices for b in devices)
-    _mailboxes[key] = ok
+    _capable.setdefault(id(g), []).append((g, ok))
     return ok
 
 
