@@ -69,3 +69,30 @@ def test_product_never_imports_the_oracle():
     for py in pkg.rglob("*.py"):
         text = py.read_text()
         assert "import oracle" not in text and "from oracle" not in text, py
+
+
+def _build_c_client(tmp_path):
+    exe = tmp_path / "abi_client"
+    subprocess.run(["cc", "-std=c11", "-O2", "-Wall", "-Werror", f"-I{HEADER.parent}",
+                    str(Path(__file__).resolve().parent / "c" / "abi_client.c"),
+                    f"-L{_runtime.LIB_PATH.parent}", "-lrtcg_b200",
+                    f"-Wl,-rpath,{_runtime.LIB_PATH.parent}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_client_compiles_through_the_abi(tmp_path):
+    """A plain C program linked against librtcg_b200.so (no Python) gets an
+    sm_100a cubin from NVRTC and a structured compile error."""
+    out = subprocess.run([str(_build_c_client(tmp_path)), "compile"], capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "cubin" in out.stdout
+
+
+@pytest.mark.gpu
+def test_c_client_launches_through_the_abi(tmp_path):
+    """The same C program loads, launches and verifies a kernel on the B200."""
+    out = subprocess.run([str(_build_c_client(tmp_path)), "run"], capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "0 mismatches" in out.stdout
