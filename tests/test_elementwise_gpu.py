@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import cport, csem
-from paper_0911_3456_b200 import _runtime, elementwise as ew, jit, ndarray as nd
+from paper_0911_3456_b200 import elementwise as ew, jit, ndarray as nd
 
 pytestmark = pytest.mark.gpu
 
