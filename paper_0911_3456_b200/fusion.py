@@ -16,6 +16,14 @@ Results are bit-identical to the eager chain: every node applies the eager
 operator's promotion and scalar rules and casts its result back to the
 promoted dtype, exactly the value the eager kernel would have stored in its
 temporary (e.g. int8 + int8 wraps to int8 before the next operator).
+
+A chain that ends in a reduction (``fusion.reduce(expr, "sum")``, or
+``fused(f, reduce="sum")``) becomes the map expression of one generated
+ReductionKernel: one HBM pass over the leaves and no materialised result.
+Integer sums and max/min equal ``gpuarray.sum/max/min(evaluate(expr))``
+bit for bit; float sums fold the same per-element values (fp64 accumulation
+for float32) and agree within the reference's fp64-accumulation bound --
+exactly when the leaves have the result's width (same chunking).
 """
 
 from __future__ import annotations
@@ -28,7 +36,7 @@ from . import elementwise as ew
 from . import ndarray as nd
 from .ndarray import DivisionByZero, NdArray, ShapeMismatch
 
-__all__ = ["Expr", "lazy", "evaluate", "fused", "kernel_count"]
+__all__ = ["Expr", "lazy", "evaluate", "reduce", "fused", "kernel_count"]
 
 _SYMBOLS = {"add": "+", "sub": "-", "mul": "*", "div": "/"}
 
@@ -182,12 +190,61 @@ def evaluate(expr, out: NdArray | None = None, stream=None) -> NdArray:
     return out
 
 
-def fused(fn):
+_REDUCE_OPS = ("sum", "max", "min")
+_reduction_memo: dict = {}
+
+
+def _reduction_for(key, arrays, scalars, dtype: nd.Dtype, op: str):
+    from . import reduction as rd
+    memo_key = (key, dtype.name, op)
+    kernel = _reduction_memo.get(memo_key)
+    if kernel is None:
+        import hashlib
+        params = [ew.KernelParam(f"rtcg_fa{k}", a.dtype, True) for k, a in enumerate(arrays)]
+        params += [ew.KernelParam(f"rtcg_fs{k}", sd, False) for k, (_, sd) in enumerate(scalars)]
+        neutral, reduce_expr = {"sum": ("0", "a + b"),
+                                "max": (rd._lowest(dtype), "a > b ? a : b"),
+                                "min": (rd._highest(dtype), "a < b ? a : b")}[op]
+        mapped = _render(key, "[i]")
+        if key[0] != "a" or arrays[key[1]].dtype is not dtype:
+            mapped = f"(({dtype.cname}) {mapped})"
+        spec = rd.ReductionSpec(ew.KernelSignature(tuple(params)), dtype, neutral, reduce_expr,
+                                mapped)
+        tag = hashlib.sha256(repr(memo_key).encode()).hexdigest()[:12]
+        kernel = rd.ReductionKernel(spec, f"fusedr_{tag}")
+        with _memo_lock:
+            kernel = _reduction_memo.setdefault(memo_key, kernel)
+    return kernel
+
+
+def reduce(expr, op: str = "sum", *, return_device: bool = True, stream=None):  # noqa: A001
+    """Reduce a traced expression (``sum`` / ``max`` / ``min``) in one pass:
+    the expression is the map of a generated ReductionKernel.  Returns a 0-d
+    GPUArray (PyCUDA style) or, with ``return_device=False``, a numpy
+    scalar."""
+    if op not in _REDUCE_OPS:
+        raise ValueError(f"op must be one of {_REDUCE_OPS}, got {op!r}")
+    if isinstance(expr, NdArray):
+        expr = lazy(expr)
+    if not isinstance(expr, Expr):
+        raise TypeError("reduce() takes an Expr or a GPUArray")
+    key, arrays, scalars = expr._leaves()
+    kernel = _reduction_for(key, arrays, scalars, expr.dtype, op)
+    return kernel(*arrays, *[v for v, _ in scalars], n=arrays[0].size,
+                  return_device=return_device, stream=stream)
+
+
+def fused(fn, reduce: str | None = None):  # noqa: A002 - keyword mirrors the function
     """Decorator: ``fused(f)(*arrays)`` traces ``f`` over lazy leaves and
-    evaluates it as one kernel."""
+    evaluates it as one kernel; ``fused(f, reduce="sum")`` reduces the traced
+    chain in the same pass (a 0-d GPUArray)."""
+    reducer = reduce
+
     def run(*args, out=None, stream=None):
         traced = fn(*(Expr(("A", a), a.dtype, a.shape) if a.__class__ is NdArray else
                       lazy(a) if isinstance(a, NdArray) else a for a in args))
+        if reducer is not None:
+            return globals()["reduce"](traced, reducer, stream=stream)
         return evaluate(traced, out=out, stream=stream)
     run.__name__ = getattr(fn, "__name__", "fused")
     return run

@@ -72,3 +72,41 @@ def test_fused_chain_is_one_launch_and_no_temporaries(pool):
     assert np.array_equal(z.get(), (np.arange(1 << 20, dtype=np.float32) + 1))
     out = pool.alloc(nd.float32, (1 << 20,))
     assert f(x, y, out=out) is out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dname", ["int8", "int32", "int64", "uint16", "float32", "float64"])
+def test_fused_reductions_match_the_eager_chain(pool, dname):
+    """reduce(chain) == gpuarray.<op>(evaluate(chain)): integer sums and
+    max/min bit for bit; float sums identical here (leaves have the result's
+    width, so the chunking and fold order are the eager sum's)."""
+    from paper_0911_3456_b200 import gpuarray as ga
+    d = nd.BY_NAME[dname]
+    rng = np.random.default_rng(12)
+    n = 1_000_003
+    hx = rng.integers(-50, 50, n).astype(d.np) if d.kind != "f" else \
+        rng.uniform(-1, 1, n).astype(d.np)
+    hy = rng.integers(0, 7, n).astype(d.np) if d.kind != "f" else \
+        rng.uniform(-1, 1, n).astype(d.np)
+    x, y = nd.from_host(pool, d, hx), nd.from_host(pool, d, hy)
+    chain = (fusion.lazy(x) * 3 + y) - x
+    eager = fusion.evaluate(chain)
+    for op, ref in (("sum", ga.sum), ("max", ga.max), ("min", ga.min)):
+        got = fusion.reduce(chain, op).get()
+        want = ref(eager).get()
+        assert got.dtype == want.dtype and got.tobytes() == want.tobytes(), (op, got, want)
+    f = fusion.fused(lambda p, q: p * q, reduce="sum")
+    assert f(x, y).get().tobytes() == ga.sum(x * y).get().tobytes()
+
+
+@pytest.mark.gpu
+def test_fused_reduction_is_one_pass_without_temporaries(pool):
+    n = 1 << 22
+    x = nd.from_host(pool, nd.float32, np.ones(n, np.float32))
+    y = nd.from_host(pool, nd.float32, np.full(n, 2.0, np.float32))
+    before = pool.stats()["allocations_served"]
+    r = fusion.reduce(fusion.lazy(x) * 2.5 + y, "sum", return_device=False)
+    assert pool.stats()["allocations_served"] == before        # no temporaries, host scalar
+    assert float(r) == 4.5 * n and isinstance(r, np.float64)   # Python float scalar -> f64
+    with pytest.raises(ValueError):
+        fusion.reduce(fusion.lazy(x), "prod")
