@@ -149,6 +149,14 @@ def main():
                 rec("chain_eager", eager, 3 * sz * n)   # algorithmic: read x, y; write z
             f = fusion.fused(lambda p, q: (p * 2 + q) - p)
             rec("chain_fused", lambda: f(x, y, out=z), 3 * sz * n)
+            fr = fusion.fused(lambda p, q: (p * 2 + q) - p, reduce="sum")
+
+            def chain_then_sum():
+                f(x, y, out=z)
+                sm.launch(z, out=o)
+            # chain + reduction: algorithmic bytes = the two inputs
+            rec("chain_sum_two_pass", chain_then_sum, 2 * sz * n)
+            rec("chain_sum_fused", lambda: fr(x, y).free(), 2 * sz * n)
             rec("sum", lambda: sm.launch(x, out=o), sz * n)
             rec("max", lambda: mx.launch(x, out=o), sz * n)
             rec("dot", lambda: dot.launch(x, y, out=o), 2 * sz * n)
