@@ -1,0 +1,75 @@
+"""Streamed host calls (``driver.In`` / ``Out`` / ``InOut``): chunked
+upload / kernel / download on two streams must give exactly the result of
+the resident path, for pageable and page-locked host arrays, mixed with
+GPUArray arguments, at chunk edges and with shard bases."""
+
+import numpy as np
+import pytest
+
+from oracle import cport
+from paper_0911_3456_b200 import driver as drv, elementwise as ew, ndarray as nd
+
+pytestmark = pytest.mark.gpu
+
+AXPY = ("float a, float *x, float b, float *y, float *z", "z[i] = a * x[i] + b * y[i]")
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("chunk", [None, 1 << 16, 99_999])
+def test_axpy_host_in_out_equals_oracle(kernel_env, pinned, chunk):
+    kwargs, pool = kernel_env
+    n = 1_000_003
+    rng = np.random.default_rng(3)
+    if pinned:
+        x, y, z = (nd.pinned_empty((n,), nd.float32) for _ in range(3))
+        x[:] = rng.uniform(-1, 1, n)
+        y[:] = rng.uniform(-1, 1, n)
+    else:
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        y = rng.uniform(-1, 1, n).astype(np.float32)
+        z = np.zeros(n, np.float32)
+    k = ew.make_elementwise(*AXPY, "axpy_host", **kwargs)
+    k._call_host((2.0, drv.In(x), -3.0, drv.In(y), drv.Out(z)), None, chunk=chunk) if chunk \
+        else k(2.0, drv.In(x), -3.0, drv.In(y), drv.Out(z))
+    want = np.zeros(n, np.float32)
+    cport.Elementwise(*AXPY)(2.0, np.asarray(x), -3.0, np.asarray(y), want)
+    assert np.array_equal(np.asarray(z), want)
+
+
+def test_inout_mixed_with_device_arrays_and_global_index(kernel_env):
+    kwargs, pool = kernel_env
+    n = 300_001
+    host = np.arange(n, dtype=np.int64)
+    dev = nd.from_host(pool, nd.int64, np.full(n, 7, np.int64))
+    k = ew.make_elementwise("long *h, long *d", "h[i] = h[i] * 2 + d[i] + i", "mix_host", **kwargs)
+    k._call_host((drv.InOut(host), dev), None, chunk=65_536)
+    assert np.array_equal(host, np.arange(n) * 3 + 7)
+
+
+def test_explicit_n_and_errors(kernel_env):
+    kwargs, pool = kernel_env
+    k = ew.make_elementwise(*AXPY, "axpy_host_err", **kwargs)
+    x = np.ones(1000, np.float32)
+    z = np.zeros(1000, np.float32)
+    k(1.0, drv.In(x), 1.0, drv.In(x), drv.Out(z), n=10)
+    assert np.all(z[:10] == 2.0) and np.all(z[10:] == 0.0)
+    with pytest.raises(ew.DtypeMismatch):
+        k(1.0, drv.In(x.astype(np.float64)), 1.0, drv.In(x), drv.Out(z))
+    with pytest.raises(ew.DtypeMismatch):
+        k(drv.In(x), drv.In(x), 1.0, drv.In(x), drv.Out(z))
+    with pytest.raises(nd.ShapeMismatch):
+        k(1.0, drv.In(x[:5]), 1.0, drv.In(x), drv.Out(z))
+    with pytest.raises(ValueError):
+        drv.Out(np.ones(4, np.float32)[::2])
+
+
+def test_views_share_storage(kernel_env):
+    kwargs, pool = kernel_env
+    a = nd.from_host(pool, nd.int32, np.arange(100, dtype=np.int32))
+    v = a[10:20]
+    ew.make_elementwise("int *x", "x[i] = -x[i]", "neg_view", **kwargs)(v)
+    got = a.get()
+    assert np.array_equal(got[10:20], -np.arange(10, 20)) and got[9] == 9 and got[20] == 20
+    assert np.array_equal((v + 1).get(), -np.arange(10, 20) + 1)
+    with pytest.raises(ValueError):
+        v.free()
