@@ -522,21 +522,30 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
     # CPU kernel on all host cores -- the compute-heavy case where the GPU wins
     # end to end even though every byte crosses PCIe.
     hz = nd.pinned_empty((n,), nd.float64)
+    from paper_0911_3456_b200 import driver as drv
 
-    def e2e():
+    def e2e_sequential():
         xd.copy_from_host(hx, sync=False)
         ps(0.5, xd, zd)
         zd.to_host(out=hz)
-    e2e()
-    reps = 3
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        e2e()
-    e2e_s = (time.perf_counter() - t0) / reps
+
+    def e2e_streamed():           # chunked upload / kernel / download on two streams
+        ps(0.5, drv.In(hx), drv.Out(hz))
+
+    def timed(fn, reps=3):
+        fn()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        return (time.perf_counter() - t0) / reps
+    seq_s, str_s = timed(e2e_sequential), timed(e2e_streamed)
     out["polysin_f64_2p28"]["e2e"] = {
-        "value": round(16 * n / e2e_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
-        "d2h_bytes_per_step": 8 * n, "steps": reps,
-        "path": "GPUArray.copy_from_host (pinned) + ElementwiseKernel + GPUArray.to_host (pinned)"}
+        "value": round(16 * n / str_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
+        "d2h_bytes_per_step": 8 * n, "steps": 3,
+        "path": "ElementwiseKernel(0.5, driver.In(x), driver.Out(z)) on pinned host arrays: "
+                "32 MiB chunks, upload / kernel / download overlapped on two streams",
+        "sequential_value": round(16 * n / seq_s / 1e9, 2),
+        "sequential_path": "GPUArray.copy_from_host + ElementwiseKernel + GPUArray.to_host"}
     try:
         from oracle import refdrive
         fn, kind = refdrive.load("polysin")
