@@ -58,7 +58,7 @@ def test_explicit_n_and_errors(kernel_env):
     with pytest.raises(ew.DtypeMismatch):
         k(drv.In(x), drv.In(x), 1.0, drv.In(x), drv.Out(z))
     with pytest.raises(nd.ShapeMismatch):
-        k(1.0, drv.In(x[:5]), 1.0, drv.In(x), drv.Out(z))
+        k(1.0, drv.In(x), 1.0, drv.In(x[:5]), drv.Out(z))   # n = first vector's size
     with pytest.raises(ValueError):
         drv.Out(np.ones(4, np.float32)[::2])
 
