@@ -485,7 +485,7 @@ def registers(function: int) -> int:
 def launch(function: int, grid: int, block: int, params, smem: int = 0,
            stream: int | None = None) -> None:
     """cuLaunchKernel with ``params`` = ctypes array of pointers to values."""
-    s = current_stream() if stream is None else stream
+    s = current_stream() if stream is None else getattr(stream, "handle", stream)
     _check(lib().rtcg_launch(function, grid, block, smem, s or None, params),
            "launch")
 

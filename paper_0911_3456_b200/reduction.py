@@ -322,7 +322,8 @@ class ReductionKernel:
             dev = getattr(tls, "device", None)
             if dev is None:
                 dev = _runtime.current_device()
-            st = getattr(tls, "stream", 0) if stream is None else stream
+            st = getattr(tls, "stream", 0) if stream is None else \
+                getattr(stream, "handle", stream) or 0
             s = self._scratch.get((dev, st)) or self.scratch(dev, st)
             plan = self._plans.get(dev) or self._plan(dev)
             got = plan.launch(args, n, base, st or 0, s.capacity,

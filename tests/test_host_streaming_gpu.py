@@ -73,3 +73,18 @@ def test_views_share_storage(kernel_env):
     assert np.array_equal((v + 1).get(), -np.arange(10, 20) + 1)
     with pytest.raises(ValueError):
         v.free()
+
+
+def test_stream_objects_and_handles_are_accepted(kernel_env):
+    from paper_0911_3456_b200 import _runtime, reduction as rd
+    kwargs, pool = kernel_env
+    st = _runtime.Stream()
+    x = nd.from_host(pool, nd.float32, np.arange(1000, dtype=np.float32))
+    z = pool.alloc(nd.float32, (1000,))
+    k = ew.make_elementwise("float *x, float *z", "z[i] = x[i] + 1", "plus1_st", **kwargs)
+    k(x, z, stream=st)
+    k(x, z, stream=st.handle)
+    st.synchronize()
+    assert np.array_equal(z.get(), np.arange(1000) + 1)
+    s = rd.sum_kernel(nd.float32, **kwargs)
+    assert float(s(x, stream=st)) == float(np.arange(1000).sum())
