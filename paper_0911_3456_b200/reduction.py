@@ -246,10 +246,13 @@ class ReductionKernel:
                 return self.vectorized, self.variant.unroll * self.width, 0
         return self.generic, self.variant.unroll, 0
 
-    def _read(self, address: int, dtype: Dtype):
+    def _read(self, address: int, dtype: Dtype, stream=None):
+        """Read one value on ``stream`` (default: the current stream) -- the
+        stream the producing kernel ran on, so the copy is ordered after it."""
+        st = None if stream is None else getattr(stream, "handle", stream)
         box = nd.ctype_for(dtype)()
-        _runtime.memcpy_dtoh(ctypes.addressof(box), address, dtype.size)
-        _runtime.stream_synchronize()
+        _runtime.memcpy_dtoh(ctypes.addressof(box), address, dtype.size, st)
+        _runtime.stream_synchronize(st)
         return dtype.np.type(box.value)
 
     def _launch_combine(self, partials: int, count: int, result: int, out: int,
@@ -317,13 +320,14 @@ class ReductionKernel:
         exchanges the device accumulator with every rank over peer memory and
         result/out receive the global value (every rank must make the same
         call; an empty local span still takes part)."""
+        if stream is not None:
+            stream = getattr(stream, "handle", stream)
         if peers is None:
             tls = _runtime._tls
             dev = getattr(tls, "device", None)
             if dev is None:
                 dev = _runtime.current_device()
-            st = getattr(tls, "stream", 0) if stream is None else \
-                getattr(stream, "handle", stream) or 0
+            st = getattr(tls, "stream", 0) if stream is None else stream or 0
             s = self._scratch.get((dev, st)) or self.scratch(dev, st)
             plan = self._plans.get(dev) or self._plan(dev)
             got = plan.launch(args, n, base, st or 0, s.capacity,
@@ -397,7 +401,7 @@ class ReductionKernel:
             self.launch(*args, n=n, base=base, stream=stream, out=out)
             return out
         s = self.launch(*args, n=n, base=base, stream=stream)
-        return self._read(s.out, self.spec.out_dtype)
+        return self._read(s.out, self.spec.out_dtype, stream)
 
 
 def make_reduction(signature, out_dtype, neutral: str, reduce_expr: str,
