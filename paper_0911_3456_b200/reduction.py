@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes
 import re
 import threading
+from threading import get_ident as _get_ident
 from dataclasses import dataclass
 
 import numpy as np
@@ -224,9 +225,12 @@ class ReductionKernel:
     # -- plumbing --
 
     def scratch(self, device: int, stream: int | None = None) -> _Scratch:
-        """Partials / result / ticket buffers for (device, stream): launches on
-        different streams never share a ticket."""
-        key = (device, _runtime.current_stream() if stream is None else stream)
+        """Partials / result / ticket buffers for (device, stream, calling
+        thread): launches on different streams never share a ticket, and two
+        threads sharing a kernel object and a stream never read each other's
+        result (the reference's kernels are shareable between threads,
+        SPEC:331)."""
+        key = (device, _runtime.current_stream() if stream is None else stream, _get_ident())
         with self._lock:
             s = self._scratch.get(key)
             if s is None:
@@ -328,7 +332,7 @@ class ReductionKernel:
             if dev is None:
                 dev = _runtime.current_device()
             st = getattr(tls, "stream", 0) if stream is None else stream or 0
-            s = self._scratch.get((dev, st)) or self.scratch(dev, st)
+            s = self._scratch.get((dev, st, _get_ident())) or self.scratch(dev, st)
             plan = self._plans.get(dev) or self._plan(dev)
             got = plan.launch(args, n, base, st or 0, s.capacity,
                               (s.partials, s.result, s.out if out is None else out.address,

@@ -239,3 +239,21 @@ def test_c4_full_size_closed_forms(kernel_env):
                          "axpb_c4", **kwargs)(2.0, xf, 3.0, z)
     assert float(rd.sum_kernel(nd.float32, **kwargs)(z)) == float(np.float32(
         reps * float(np.sum(2.0 * block + 3.0))))
+
+
+def test_threads_sharing_a_kernel_get_their_own_results(kernel_env):
+    """Kernel objects are shareable between threads (reference SPEC:331): 8
+    threads calling one sum kernel on the same stream each read their own
+    result, every time."""
+    from concurrent.futures import ThreadPoolExecutor
+    kwargs, pool = kernel_env
+    k = rd.sum_kernel(nd.int64, **kwargs)
+    arrays = [nd.from_host(pool, nd.int64, np.full(100_000 + t, t, np.int64)) for t in range(8)]
+    want = [t * (100_000 + t) for t in range(8)]
+
+    def worker(t):
+        from paper_0911_3456_b200 import _runtime
+        _runtime.set_device(0)
+        return all(int(k(arrays[t])) == want[t] for _ in range(50))
+    with ThreadPoolExecutor(8) as ex:
+        assert all(ex.map(worker, range(8)))
