@@ -274,3 +274,20 @@ def test_auto_kernels_tune_once_per_bucket(pool, tmp_path, shared_cache):
     assert float(r(x)) == 8000.0 and len(r.results) == 1
     again = at.AutoReduction(spec, "auto_sum", axes, store=store, cache=shared_cache, pool=pool)
     assert float(again(x)) == 8000.0 and again.results[8192].from_store
+
+
+def test_algorithmic_bytes_follow_the_access_analysis():
+    import ctypes
+    from paper_0911_3456_b200 import elementwise as ew, ndarray as nd, reduction as rd
+    pool = nd.MemoryPool(lambda n: ctypes.create_string_buffer(n), zero_fill=lambda a, n: None)
+    x, y, z = (pool.alloc(nd.float32, (1000,)) for _ in range(3))
+    axpy = ew.ElementwiseKernel("float a, float *x, float b, float *y, float *z",
+                                "z[i] = a * x[i] + b * y[i]", "axpy_bytes")
+    assert at.algorithmic_bytes(axpy, 2.0, x, 3.0, y, z) == 12_000
+    inplace = ew.ElementwiseKernel("float *x, float *z", "z[i] += x[i]", "inplace_bytes")
+    assert at.algorithmic_bytes(inplace, x, z) == 12_000          # z read and written
+    assert at.algorithmic_bytes(inplace, x, z, n=10) == 120
+    dot = rd.dot_kernel(nd.float32)
+    assert at.algorithmic_bytes(dot, x, y) == 8_000
+    peak, kind = at.measured_hbm_gbs()
+    assert peak > 1000 and kind in ("measured", "fallback")

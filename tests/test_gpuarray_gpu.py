@@ -112,3 +112,17 @@ def test_pinned_and_pageable_paths_agree(pool):
     out_pin = nd.pinned_empty((n,), nd.int64)
     a.to_host(out=out_pin)
     assert np.array_equal(out_pin, h) and np.array_equal(b.get(), h)
+
+
+def test_roofline_helper_reports_hbm_fraction(pool):
+    from paper_0911_3456_b200 import autotune as at, elementwise as ew, reduction as rd
+    n = 1 << 26
+    x = pool.alloc(nd.float32, (n,))
+    y = pool.alloc(nd.float32, (n,))
+    z = pool.alloc(nd.float32, (n,))
+    axpy = ew.ElementwiseKernel("float a, float *x, float b, float *y, float *z",
+                                "z[i] = a * x[i] + b * y[i]", "axpy_roof")
+    r = at.roofline(axpy, 2.0, x, -3.0, y, z)
+    assert r["bytes"] == 12 * n and r["GB/s"] > 3000 and 0.4 < r["frac"] < 1.3
+    d = at.roofline(rd.dot_kernel(nd.float32), x, y)
+    assert d["bytes"] == 8 * n and d["GB/s"] > 3000
