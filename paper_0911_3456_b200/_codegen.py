@@ -55,6 +55,29 @@ TMA_STAGE_BYTES = 32 * 1024
 TMA_HEADER = 128
 
 
+TMA_SMEM_BUDGET = 200 * 1024   # of the 227 KB a CTA may opt in to
+
+
+def _tma_layout(sig, access, width: int, block: int | None, staged: str):
+    """(staged vectors, tile elements, stages) or None when no ring of >= 2
+    stages fits the shared-memory budget."""
+    pick = (lambda a: a.used) if staged == "used" else (lambda a: a.read)
+    used = [p for p in sig.vectors if pick(access[p.name])]
+    per_elem = sum(p.dtype.size for p in used)
+    if not used:
+        return None
+    if block is None:
+        tile = max(width * 16, (TMA_STAGE_BYTES // per_elem) // width * width)
+    else:
+        consumers = block - 32
+        per_thread = max(1, TMA_STAGE_BYTES // (consumers * width * per_elem))
+        tile = per_thread * consumers * width
+    stages = min(TMA_STAGES, (TMA_SMEM_BUDGET - TMA_HEADER) // (tile * per_elem))
+    if stages < 2:
+        return None
+    return used, tile, stages
+
+
 def tma_parts(sig, access, width: int, block: int | None = None,
               staged: str = "used") -> dict:
     """Bindings of a template's TMA path: shared-memory rings (one per staged
@@ -66,16 +89,10 @@ def tma_parts(sig, access, width: int, block: int | None = None,
     written vectors are stored straight from registers) and size the tile so
     every consumer thread (all warps but the producer) owns the same number of
     16-byte chunks -- an uneven split idles consumers on compute-heavy
-    statements."""
-    pick = (lambda a: a.used) if staged == "used" else (lambda a: a.read)
-    used = [p for p in sig.vectors if pick(access[p.name])]
+    statements.  The ring has up to 4 stages, fewer when a tile of wide
+    vectors is large (at least 2, see :func:`tma_eligible`)."""
+    used, tile, stages = _tma_layout(sig, access, width, block, staged)
     per_elem = sum(p.dtype.size for p in used)
-    if block is None:
-        tile = max(width * 16, (TMA_STAGE_BYTES // per_elem) // width * width)
-    else:
-        consumers = block - 32
-        per_thread = max(1, TMA_STAGE_BYTES // (consumers * width * per_elem))
-        tile = per_thread * consumers * width
     rings, bulks, loads = [], [], []
     offset = 0
     for p in used:
@@ -85,16 +102,19 @@ def tma_parts(sig, access, width: int, block: int | None = None,
                      f"rtcg_p_{p.name} + t * TE, (unsigned)(TE * sizeof({c})), rtcg_full + s);")
         loads.append(f"                    rtcg::tma::load_smem(rtcg_v_{p.name}[u], "
                      f"rtcg_r_{p.name} + s * TE, c);")
-        offset += TMA_STAGES * tile * p.dtype.size
-    return {"tma": True, "stages": TMA_STAGES, "tile": tile, "tile_bytes": tile * per_elem,
+        offset += stages * tile * p.dtype.size
+    return {"tma": True, "stages": stages, "tile": tile, "tile_bytes": tile * per_elem,
             "ring_decls": "\n".join(rings), "bulk_loads": "\n".join(bulks),
             "smem_loads": "\n".join(loads), "tma_smem": TMA_HEADER + offset}
 
 
-def tma_eligible(sig, access, width: int) -> bool:
-    """An elementwise TMA path needs the vector path and something to stage."""
-    return (access is not None and width > 0
-            and any(access[p.name].read for p in sig.vectors))
+def tma_eligible(sig, access, width: int, block: int | None = None,
+                 staged: str = "read") -> bool:
+    """A TMA path needs the vector path, something to stage and a ring of at
+    least two stages within the shared-memory budget."""
+    if access is None or width <= 0:
+        return False
+    return _tma_layout(sig, access, width, block, staged) is not None
 
 _CONTROL = re.compile(r"\b(?:if|else|for|while|do|switch|case|goto|return|break|continue)\b|[{}]")
 

@@ -152,3 +152,22 @@ def test_user_names_that_match_template_locals(kernel_env, cache):
                   pool.alloc(nd.float32, (n,)))
     k(1.25, gc, -0.5, gb, gs)
     assert np.array_equal(gs.to_host(), np.float32(1.25) * c + np.float32(-0.5) * b)
+
+
+@pytest.mark.parametrize("block", [64, 256, 1024])
+def test_wide_tiles_shrink_or_fall_back_to_ldg(kernel_env, block):
+    """int8 + double chunks are 16 elements (144 staged bytes per chunk): at
+    block 1024 one chunk per consumer already exceeds the shared-memory budget
+    for a 2-stage ring, so the variant keeps the LDG path; smaller blocks use
+    the ring.  Results are identical either way."""
+    kwargs, pool = kernel_env
+    n = 250_007
+    rng = np.random.default_rng(6)
+    b = rng.integers(-9, 9, n).astype(np.int8)
+    x = rng.uniform(-1, 1, n)
+    k = ew.make_elementwise("int8_t *b, double *x, double *z", "z[i] = b[i] * x[i]", "wide",
+                            ew.VariantParams(cache="tma", block=block), **kwargs)
+    assert (k.smem > 0) == (block < 1024) and k.smem <= 227 * 1024
+    gz = pool.alloc(nd.float64, (n,))
+    k(nd.from_host(pool, nd.int8, b), nd.from_host(pool, nd.float64, x), gz)
+    assert np.array_equal(gz.get(), b * x)

@@ -3,7 +3,10 @@
 Paths: elementwise vector / general (neighbour access, aliasing, misaligned),
 head/tail splits, contiguous + strided partitions, full-grid and resident
 waves; reductions vector / general / TMA / combine / empty span / multi-CTA
-last-block fold; fused chains; a captured graph.
+last-block fold; fused chains and fused chain+reduction; a captured graph;
+elementwise TMA rings (read, read-write, mixed widths, tile edges); the
+cross-rank peer exchange with emulated ranks on their own streams; views and
+streamed host calls (driver.In/Out).
 """
 import sys
 from pathlib import Path
@@ -41,6 +44,45 @@ for n in (1, 5, 37, 1000, 65_539):
     fusion.fused(lambda p, q: (p * 2 + q) - p)(x, y)
     checks += 6
 float(rd.sum_kernel(nd.float64)(pool.alloc(nd.float64, (0,))))     # empty span -> combine
+# elementwise TMA rings
+from paper_0911_3456_b200 import driver as drv, parallel as par  # noqa: E402
+for n in (1, 37, 20_000, 100_003):
+    a = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
+    b8 = nd.from_host(pool, nd.int8, rng.integers(-9, 9, n).astype(np.int8))
+    c = pool.alloc(nd.float64, (n,))
+    for blk in (64, 256, 1024):
+        tv = ew.VariantParams(cache="tma", block=blk)
+        ew.ElementwiseKernel("double *x, double *z", "z[i] = x[i] * 2 + sin(x[i])", "tps", tv)(a, c)
+        ew.ElementwiseKernel("double *x, double *z", "z[i] += x[i]", "trw", tv)(a, c)
+        ew.ElementwiseKernel("int8_t *b, double *x, double *z", "z[i] = b[i] * x[i]", "tmx",
+                             tv)(b8, a, c)
+        checks += 3
+    fusion.reduce(fusion.lazy(a) * 2 - a, "sum").get()
+    a[n // 3:n // 2 + 1] * 2.0
+    checks += 2
+# peer exchange, 3 emulated ranks on their own streams
+xs = rng.integers(-100, 100, 90_001).astype(np.int64)
+group = par.PeerMailbox.local_group(3)
+streams = [rt.Stream() for _ in range(3)]
+ks = rd.sum_kernel(nd.int64)
+parts = [nd.from_host(pool, nd.int64, xs[r * 30_000:(r + 1) * 30_000 + (r == 2)])
+         for r in range(3)]
+for _ in range(3):
+    for r in range(3):
+        with rt.use_stream(streams[r].handle):
+            ks.launch(parts[r], base=r * 30_000, peers=group[r])
+for st in streams:
+    st.synchronize()
+assert all(int(ks._read(ks.scratch(0, st.handle).result, nd.int64)) == int(xs.sum())
+           for st in streams)
+checks += 9
+# streamed host call
+hx = rng.uniform(-1, 1, 300_001).astype(np.float32)
+hz = np.zeros_like(hx)
+axs = ew.ElementwiseKernel("float *x, float *z", "z[i] = x[i] * 3", "hs")
+axs._call_host((drv.In(hx), drv.Out(hz)), None, chunk=65_536)
+assert np.array_equal(hz, hx * np.float32(3))
+checks += 5
 g = graph.Graph()
 big = nd.from_host(pool, nd.int64, np.arange(1 << 20, dtype=np.int64))
 o = pool.alloc(nd.int64, ())
