@@ -31,8 +31,8 @@ from __future__ import annotations
 import ctypes
 import re
 import threading
-from threading import get_ident as _get_ident
 from dataclasses import dataclass
+from threading import get_ident as _get_ident
 
 import numpy as np
 
@@ -40,8 +40,10 @@ from . import _runtime
 from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
-from .elementwise import (_CHUNK_TOKEN, _ERRORS, KernelSignature, ParseError, VariantParams,
-                          _check_name, _preamble_text, parse_signature)
+from .driver import HostArg as _HostArg
+from .elementwise import (_CHUNK_TOKEN, _ERRORS, ArityMismatch, DtypeMismatch, KernelSignature,
+                          ParseError, VariantParams, _check_name, _preamble_text,
+                          parse_signature)
 from .ndarray import Dtype
 
 __all__ = [
@@ -396,9 +398,89 @@ class ReductionKernel:
         return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n,
                 "smem": smem}
 
+    HOST_CHUNK_BYTES = 32 << 20
+
+    def _call_host(self, args, n, base: int, want_device: bool, chunk: int | None = None):
+        """Reduction over host arrays (``driver.In``): chunk j's uploads and
+        stage-1+2 reduction run on one of two streams (uploads overlap the
+        previous chunk's kernel); each chunk's accumulator lands in slot j of
+        a device array, and the compiled combine folds the slots in chunk
+        order -- the reference's ordered fold of worker partials with chunks
+        as workers (src/reduction.py:211-216)."""
+        from .driver import HostArg
+        from .elementwise import _host_streams
+        params = self.spec.signature.params
+        if len(args) != len(params):
+            raise ArityMismatch(f"kernel {self.name} takes {len(params)} arguments, "
+                                f"got {len(args)}")
+        host_bytes = 0
+        for p, a in zip(params, args):
+            if isinstance(a, HostArg):
+                if not p.is_vector:
+                    raise DtypeMismatch(p.name, "a host array passed for a scalar")
+                if a.copy_out:
+                    raise ValueError("reductions take host inputs only (driver.In)")
+                if a.array.dtype != p.dtype.np:
+                    raise DtypeMismatch(p.name, f"expected dtype {p.dtype.name}, "
+                                                f"got {a.array.dtype}")
+                host_bytes += p.dtype.size
+        first = next((a for p, a in zip(params, args) if p.is_vector), None)
+        total = n if n is not None else first.size
+        for p, a in zip(params, args):
+            if p.is_vector and a.size < total:
+                raise nd.ShapeMismatch(f"vector {p.name!r} holds {a.size} elements, "
+                                       f"kernel span is {total}")
+        dev = _runtime.current_device()
+        pool = nd.default_pool(dev)
+        out = pool.alloc_uninitialized(self.spec.out_dtype, ())
+        step = chunk or max(1 << 16, self.HOST_CHUNK_BYTES // max(1, host_bytes) // 256 * 256)
+        step = max(1, min(step, total)) if total > 0 else 1
+        count = -(-total // step) if total > 0 else 0
+        accs = pool.alloc_uninitialized(self.spec.acc_dtype, (max(1, count),))
+        streams = _host_streams(dev)
+        staging = [[pool.alloc_uninitialized(p.dtype, (step,)) if isinstance(a, HostArg)
+                    else None for p, a in zip(params, args)] for _ in streams]
+        acc_size = self.spec.acc_dtype.size
+        try:
+            for j in range(count):
+                lo, hi = j * step, min(total, (j + 1) * step)
+                k = j % len(streams)
+                st = streams[k]
+                call = []
+                with _runtime.use_stream(st.handle):
+                    for p, a, buf in zip(params, args, staging[k]):
+                        if isinstance(a, HostArg):
+                            _runtime.copy_htod(buf.address, a.array[lo:hi].ctypes.data,
+                                               (hi - lo) * p.dtype.size)
+                            call.append(buf)
+                        elif p.is_vector:
+                            call.append(a[lo:hi])
+                        else:
+                            call.append(a)
+                    s = self.launch(*call, n=hi - lo, base=base + lo)
+                    _runtime.memcpy_dtod(accs.address + j * acc_size, s.result, acc_size)
+            for st in streams:
+                st.synchronize()
+            s = self.scratch(dev)
+            s.ensure(1)
+            self._launch_combine(accs.address, count, s.result, out.address)
+            if want_device:
+                return out
+            value = self._read(out.address, self.spec.out_dtype)
+            out.free()
+            return value
+        finally:
+            accs.free()
+            for stage in staging:
+                for buf in stage:
+                    if buf is not None:
+                        buf.free()
+
     def __call__(self, *args, n: int | None = None, stream=None,
                  return_device: bool | None = None, base: int = 0):
         want_device = self.return_device if return_device is None else return_device
+        if any(isinstance(a, _HostArg) for a in args):
+            return self._call_host(args, n, base, want_device)
         if want_device:
             first = next(a for a, p in zip(args, self.spec.signature.params) if p.is_vector)
             out = first.pool.alloc_uninitialized(self.spec.out_dtype, ())

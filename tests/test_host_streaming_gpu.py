@@ -88,3 +88,34 @@ def test_stream_objects_and_handles_are_accepted(kernel_env):
     assert np.array_equal(z.get(), np.arange(1000) + 1)
     s = rd.sum_kernel(nd.float32, **kwargs)
     assert float(s(x, stream=st)) == float(np.arange(1000).sum())
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_reduction_over_host_inputs(kernel_env, pinned):
+    """dot(driver.In(x), driver.In(y)): chunked uploads, one reduction per
+    chunk, chunk accumulators folded in order -- within the fp64-accumulation
+    bound of the resident result; integer sums exact."""
+    from oracle import csem
+    from paper_0911_3456_b200 import reduction as rd
+    kwargs, pool = kernel_env
+    n = 3_000_017
+    rng = np.random.default_rng(9)
+    if pinned:
+        x, y = nd.pinned_empty((n,), nd.float32), nd.pinned_empty((n,), nd.float32)
+        x[:] = rng.uniform(-1, 1, n)
+        y[:] = rng.uniform(-1, 1, n)
+    else:
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        y = rng.uniform(-1, 1, n).astype(np.float32)
+    dot = rd.dot_kernel(nd.float32, **kwargs)
+    got = float(dot(drv.In(x), drv.In(y)))
+    terms = (np.asarray(x) * np.asarray(y)).astype(np.float64)
+    assert abs(got - csem.exact_sum(terms)) <= csem.float_reduction_bound(terms, "float32")
+    dev = dot(drv.In(x), drv.In(y), return_device=True)
+    assert float(dev.get()) == got                       # deterministic chunk order
+    ints = rng.integers(-(1 << 40), 1 << 40, n)
+    s = rd.sum_kernel(nd.int64, **kwargs)
+    assert int(s._call_host((drv.In(ints),), None, 0, False, chunk=123_457)) == int(ints.sum())
+    assert int(s(drv.In(ints[:0]))) == 0                 # empty: the neutral
+    with pytest.raises(ValueError):
+        s(drv.Out(np.zeros(4, np.int64)))
