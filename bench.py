@@ -380,10 +380,11 @@ def run_ours(args) -> int:
             for _ in range(e2e_steps):
                 fn()
             return d.max((time.perf_counter() - t0) / e2e_steps)
-        seq_s = time_e2e(e2e_sequential)
-        # the streamed host call is a single-GPU API; at N > 1 the per-rank
-        # slices travel by copy_from_host and combine with the p2p exchange
-        e2e_s = seq_s if d.distributed else time_e2e(e2e_streamed)
+        # copy-in then reduce: the inputs cross the link once, whole (the
+        # measured best for a one-way workload; the streamed host call adds
+        # per-chunk overhead and is reported beside it at N = 1)
+        e2e_s = time_e2e(e2e_sequential)
+        streamed_s = None if d.distributed else time_e2e(e2e_streamed)
         e2e_gbs = 8 * total_n / e2e_s / 1e9
         # the link roofline for e2e: raw pinned HtoD copy of the same bytes
         t0 = time.perf_counter()
@@ -422,12 +423,13 @@ def run_ours(args) -> int:
                      "avg_kernel_ms": round(kern_ms, 4)},
         "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 4, "steps": e2e_steps,
-                "path": ("GPUArray.copy_from_host (pinned) x2 + sharded_reduce (numpy scalar)"
-                         if d.distributed else
-                         "ReductionKernel(driver.In(x), driver.In(y)) on pinned host arrays: "
-                         "32 MiB chunks, uploads overlapped with per-chunk reductions, numpy "
-                         "scalar result"),
-                "sequential_value": round(8 * total_n / seq_s / 1e9, 2),
+                "path": "GPUArray.copy_from_host (pinned) x2 + "
+                        + ("sharded_reduce" if d.distributed else "ReductionKernel.__call__")
+                        + " (numpy scalar)",
+                "streamed_value": None if streamed_s is None else
+                round(8 * total_n / streamed_s / 1e9, 2),
+                "streamed_path": "ReductionKernel(driver.In(x), driver.In(y)): 32 MiB chunks, "
+                                 "uploads overlapped with per-chunk reductions",
                 "link_h2d_gbs": round(link_gbs, 2),
                 "link_frac": round(e2e_gbs / (link_gbs * d.world), 4),
                 "note": "every input byte crosses the host link once per step, so e2e is "
