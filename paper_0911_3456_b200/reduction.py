@@ -40,11 +40,13 @@ from . import _runtime
 from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
-from .driver import HostArg as _HostArg
+from .driver import HostArg as _HostArg, In as _In, InOut as _InOut, Out as _Out
 from .elementwise import (_CHUNK_TOKEN, _ERRORS, ArityMismatch, DtypeMismatch, KernelSignature,
                           ParseError, VariantParams, _check_name, _preamble_text,
                           parse_signature)
 from .ndarray import Dtype
+
+_HOST_CLASSES = frozenset({_HostArg, _In, _Out, _InOut})
 
 __all__ = [
     "NonScalarResult", "ReductionSpec", "ReductionKernel", "make_reduction",
@@ -479,8 +481,9 @@ class ReductionKernel:
     def __call__(self, *args, n: int | None = None, stream=None,
                  return_device: bool | None = None, base: int = 0):
         want_device = self.return_device if return_device is None else return_device
-        if any(isinstance(a, _HostArg) for a in args):
-            return self._call_host(args, n, base, want_device)
+        for a in args:                       # host arrays: the streamed path
+            if a.__class__ in _HOST_CLASSES:
+                return self._call_host(args, n, base, want_device)
         if want_device:
             first = next(a for a, p in zip(args, self.spec.signature.params) if p.is_vector)
             out = first.pool.alloc_uninitialized(self.spec.out_dtype, ())
