@@ -219,3 +219,33 @@ def test_dropped_arrays_return_to_the_pool():
     del b
     gc.collect()
     assert pool.stats()["bytes_held"] == 4096
+
+
+def test_alloc_and_alloc_uninitialized_are_thread_safe():
+    """Every alloc() zero-fills exactly once even while other threads call
+    alloc_uninitialized() on the same pool (it used to swap the pool's zero
+    function for the duration of the call)."""
+    import ctypes
+    import threading
+    zeroed = []
+    lock = threading.Lock()
+
+    def zero(address, nbytes):
+        with lock:
+            zeroed.append(address)
+    pool = nd.MemoryPool(lambda n: ctypes.create_string_buffer(n), zero_fill=zero)
+    rounds = 2000
+
+    def zeroing():
+        for _ in range(rounds):
+            pool.alloc(nd.float32, (16,)).free()
+
+    def raw():
+        for _ in range(rounds):
+            pool.alloc_uninitialized(nd.float32, (16,)).free()
+    threads = [threading.Thread(target=f) for f in (zeroing, raw, raw, zeroing)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert len(zeroed) == 2 * rounds
