@@ -98,7 +98,9 @@ def test_random_expression_bit_exact(kernel_env, seed):
     variant = ew.VariantParams(unroll=int(rng.choice([1, 2, 4, 8])),
                                block=int(rng.choice([64, 256, 1024])),
                                chunking=str(rng.choice(ew.CHUNKINGS)),
-                               waves=int(rng.choice([0, 1, 2])))
+                               waves=int(rng.choice([0, 1, 2])),
+                               cache=str(rng.choice(["default", "default", "streaming",
+                                                     "no-l1", "l2-256", "tma"])))
     k = ew.ElementwiseKernel(sig, op, f"fz{seed}", variant, **kwargs)
     dev = [nd.from_host(pool, nd.BY_NAME[t], h) for t, h in zip(vec_types, host)]
     gd = nd.from_host(pool, nd.BY_NAME[dtype_d], d)
@@ -125,6 +127,7 @@ def test_random_map_reduction_exact_for_integers(kernel_env, seed):
     k = rd.make_reduction(f"{c} *x, {c} *y", nd.BY_NAME[t], neutral, red, expr,
                           name=f"rz{seed}", variant=ew.VariantParams(
                               unroll=int(rng.choice([1, 4, 8])),
-                              block=int(rng.choice([128, 512]))), **kwargs)
+                              block=int(rng.choice([128, 512])),
+                              cache=str(rng.choice(["default", "l2-256", "tma"]))), **kwargs)
     got = k(nd.from_host(pool, nd.BY_NAME[t], x), nd.from_host(pool, nd.BY_NAME[t], y))
     assert got == want and got.dtype == want.dtype, (expr, red)
