@@ -77,7 +77,7 @@ def _case(seed):
     return rng, sig, f"z[i] = {expr}", vec_types, sc_types, out_type, dtype_d
 
 
-@pytest.mark.parametrize("seed", range(48))
+@pytest.mark.parametrize("seed", range(128))
 def test_random_expression_bit_exact(kernel_env, seed):
     kwargs, pool = kernel_env
     rng, sig, op, vec_types, sc_types, out_type, dtype_d = _case(seed)
@@ -110,7 +110,7 @@ def test_random_expression_bit_exact(kernel_env, seed):
     assert np.array_equal(got, z_ref, equal_nan=True), (sig, op, variant)
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_map_reduction_exact_for_integers(kernel_env, seed):
     kwargs, pool = kernel_env
     rng = np.random.default_rng(1000 + seed)
