@@ -1,3 +1,5 @@
+"""Host cost of stream-ordered allocation (cuMemAllocAsync / cuMemFreeAsync)
+of a 2 GiB block on the legacy and a created stream."""
 import sys, time
 sys.path.insert(0, "/root/repo")
 from paper_0911_3456_b200 import _runtime as rt

@@ -1,3 +1,5 @@
+"""Pool allocate/free cycle times for blocks above the pooled classes (the
+stream-ordered allocator behind MemoryPool) and free/total device memory."""
 import sys, time
 sys.path.insert(0, "/root/repo")
 from paper_0911_3456_b200 import _runtime as rt, ndarray as nd
