@@ -327,6 +327,15 @@ def run_ours(args) -> int:
         # correctness of the tuned kernel on this data (cheap, before timing)
         value = kernel(gx, gy)
         terms_ok = bool(np.isfinite(value))
+        # the tuned kernel against an fp64 oracle on the same data: products
+        # rounded in float32 (C semantics), summed in float64 by numpy
+        terms = np.multiply(hx, hy, dtype=np.float32).astype(np.float64)
+        want = float(np.sum(terms))
+        bound = 0.5 * float(np.spacing(np.float32(abs(want)))) + \
+            2 * n * 2.0**-53 * float(np.abs(terms).sum())
+        check = {"got": float(value), "want_fp64": want, "bound": bound,
+                 "ok": abs(float(value) - want) <= bound}
+        del terms
 
         try:
             step()
@@ -412,7 +421,8 @@ def run_ours(args) -> int:
                    "parallelism": f"shards{d.world}" + (f"+{collective}" if d.distributed
                                                         else ""),
                    "accumulator": "float64",
-                   "gpu": info["name"], "result_finite": terms_ok},
+                   "gpu": info["name"], "result_finite": terms_ok,
+                   "result_vs_fp64_oracle": check},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
                      if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
