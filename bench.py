@@ -334,6 +334,7 @@ def run_ours(args) -> int:
         bound = 0.5 * float(np.spacing(np.float32(abs(want)))) + \
             2 * n * 2.0**-53 * float(np.abs(terms).sum())
         check = {"got": float(value), "want_fp64": want, "bound": bound,
+                 "ulps_f32": abs(float(value) - want) / float(np.spacing(np.float32(abs(want)))),
                  "ok": abs(float(value) - want) <= bound}
         del terms
 
