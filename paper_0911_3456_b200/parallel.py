@@ -38,7 +38,7 @@ from . import ndarray as nd
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
            "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op", "PeerMailbox",
-           "peer_mailbox"]
+           "PeerTimeout", "peer_mailbox"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -153,7 +153,13 @@ _NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
 # --- peer-memory exchange (the fused cross-GPU combine) -------------------------------------
 
 XR_MAX = 64                             # rtcg::XR_MAX in templates/prelude.cuh
-MAILBOX_BYTES = 8 * (XR_MAX + 2 * XR_MAX)  # epoch flags + two accumulator banks
+XR_ERROR = 3 * XR_MAX                   # rtcg::XR_ERROR: epoch of a timed-out wait
+MAILBOX_BYTES = 8 * (3 * XR_MAX + 8)    # epoch flags, two accumulator banks, error word
+
+
+class PeerTimeout(RuntimeError):
+    """A peer never published its accumulator (the kernel gave up after 20 s
+    and returned its local value)."""
 _XR = struct.Struct(f"<ii{XR_MAX}Q")     # struct rtcg::xr {int rank, world; u64 mbox[64];}
 
 
@@ -188,6 +194,18 @@ class PeerMailbox:
         with self._lock:
             self._epoch += 1
             return self._epoch
+
+    def check(self, stream=None) -> None:
+        """Synchronise ``stream`` and raise :class:`PeerTimeout` if any
+        exchange on this mailbox timed out waiting for a peer."""
+        word = ctypes.c_uint64()
+        st = 0 if stream is None else getattr(stream, "handle", stream)
+        _runtime.memcpy_dtoh(ctypes.addressof(word), self.addresses[self.rank] + 8 * XR_ERROR,
+                             8, st)
+        _runtime.stream_synchronize(st)
+        if word.value:
+            raise PeerTimeout(f"rank {self.rank}: the peer exchange of epoch {word.value} "
+                              f"timed out waiting for another rank")
 
     @staticmethod
     def _new_box() -> int:
@@ -338,6 +356,7 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
                 return out
             value = out.to_host()
             out.free()
+            mailbox.check(stream)
             return spec.out_dtype.np.type(value[()])
     with _runtime.use_stream(stream):
         scratch = kernel.launch(*local_args, n=n_local, base=base)

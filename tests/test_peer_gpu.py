@@ -220,3 +220,23 @@ def test_emulated_ranks_survive_skew_over_many_epochs(pool):
     assert got == [[want] * world] * rounds
     for m in group:
         m.close()
+
+
+def test_missing_peer_times_out_softly(pool):
+    """A rank whose peer never arrives gives up (20 s), records the epoch in
+    its error word and returns its local value; check() raises PeerTimeout
+    and the context stays usable."""
+    import time
+    from paper_0911_3456_b200 import ndarray as nd, reduction as rd
+    group = par.PeerMailbox.local_group(2)
+    x = nd.from_host(pool, nd.int64, np.arange(1000, dtype=np.int64))
+    k = rd.sum_kernel(nd.int64)
+    t0 = time.perf_counter()
+    s = k.launch(x, peers=group[0])          # rank 1 never launches
+    with pytest.raises(par.PeerTimeout):
+        group[0].check()
+    assert 15 < time.perf_counter() - t0 < 60
+    assert int(k._read(s.result, nd.int64)) == int(np.arange(1000).sum())   # local value
+    assert int(k(x)) == int(np.arange(1000).sum())                          # context alive
+    for m in group:
+        m.close()
