@@ -340,7 +340,15 @@ def run_ours(args) -> int:
 
         try:
             step()
-        except Exception as exc:  # p2p setup refused (e.g. no peer mapping): NCCL baseline
+            if collective == "p2p":   # every rank must agree the exchange works
+                timed_out = 0.0
+                try:
+                    par.peer_mailbox(None, stream_handle).check(stream_handle)
+                except par.PeerTimeout:
+                    timed_out = 1.0
+                if d.max(timed_out) > 0:
+                    raise RuntimeError("the peer exchange timed out on some rank")
+        except Exception as exc:  # p2p refused or broken here: the NCCL baseline
             if collective != "p2p":
                 raise
             print(f"warning: p2p exchange unavailable ({exc}); using NCCL", file=sys.stderr)
