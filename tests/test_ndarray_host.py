@@ -249,3 +249,35 @@ def test_alloc_and_alloc_uninitialized_are_thread_safe():
     for t in threads:
         t.join()
     assert len(zeroed) == 2 * rounds
+
+
+def test_host_argument_handlers_and_views():
+    import ctypes
+    from paper_0911_3456_b200 import driver as drv
+    a = np.arange(10, dtype=np.float32)
+    assert drv.In(a).copy_in and not drv.In(a).copy_out
+    assert drv.Out(a).copy_out and not drv.Out(a).copy_in
+    assert drv.InOut(a).copy_in and drv.InOut(a).copy_out and drv.InOut(a).size == 10
+    with pytest.raises(TypeError):
+        drv.In([1, 2, 3])
+    with pytest.raises(ValueError):
+        drv.In(a[::2])
+    ro = a.copy()
+    ro.flags.writeable = False
+    drv.In(ro)
+    with pytest.raises(ValueError):
+        drv.Out(ro)
+    pool = nd.MemoryPool(lambda n: ctypes.create_string_buffer(n), zero_fill=lambda p, n: None)
+    g = pool.alloc(nd.int32, (100,))
+    v = g[10:20]
+    assert v.size == 10 and v.address == g.address + 40 and v.pool is pool
+    assert g[-5:].size == 5 and g[90:200].size == 10 and g[50:10].size == 0
+    with pytest.raises(TypeError):
+        g[::2]
+    with pytest.raises(TypeError):
+        g[3]
+    with pytest.raises(ValueError):
+        v.free()
+    g.free()
+    with pytest.raises(ValueError):
+        g[0:1]
