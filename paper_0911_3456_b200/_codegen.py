@@ -195,6 +195,7 @@ def parts(sig, access, width: int, policy: str) -> dict:
     op_tparams, op_params, kgen, kvec, unpack = [], [], [], [], []
     ptr_gen, ptr_vec, lane_types, lane_args, call_args = [], [], [], [], []
     decls, loads, stores = [], [], []
+    decls_next, loads_next, copies_next = [], [], []
     for p in sig.params:
         c = p.dtype.cname
         if not p.is_vector:
@@ -223,6 +224,11 @@ def parts(sig, access, width: int, policy: str) -> dict:
             if acc.read:
                 hint = ld_ro if read_only else ld_rw
                 loads.append(f"                rtcg::load<{hint}>(rtcg_v_{p.name}[u], rtcg_p_{p.name}, cu);")
+                decls_next.append(f"    rtcg::chunk<{c}, E> rtcg_n_{p.name}[U];")
+                loads_next.append(f"            rtcg::load<{hint}>(rtcg_n_{p.name}[u], "
+                                  f"rtcg_p_{p.name}, cu);")
+                copies_next.append(f"#pragma unroll\n        for (int u = 0; u < U; ++u) "
+                                   f"rtcg_v_{p.name}[u] = rtcg_n_{p.name}[u];")
             if acc.written:
                 stores.append(f"                rtcg::store<{st}>(rtcg_p_{p.name}, cu, rtcg_v_{p.name}[u]);")
         else:
@@ -245,6 +251,10 @@ def parts(sig, access, width: int, policy: str) -> dict:
         "vec_decls": "\n".join(decls),
         "vec_loads": "\n".join(loads),
         "vec_stores": "\n".join(stores),
+        "vec_decls_next": "\n".join(decls_next),
+        "vec_loads_next": "\n".join(loads_next),
+        "vec_copy_next": "\n".join(copies_next),
+        "prefetch": False,
     }
 
 

@@ -27,7 +27,8 @@ _VARIANTS = (ew.VariantParams(unroll=1, block=128, chunking="contiguous-blocks")
              ew.VariantParams(unroll=4, block=256),
              ew.VariantParams(unroll=8, block=512, workers=3, chunking="contiguous-blocks"),
              ew.VariantParams(unroll=2, block=64, workers=5),
-             ew.VariantParams(cache="tma", block=128, workers=3))
+             ew.VariantParams(cache="tma", block=128, workers=3),
+             ew.VariantParams(unroll=2, block=64, workers=3, prefetch=True))
 
 
 @pytest.mark.parametrize("dname", csem.DTYPE_NAMES)
@@ -442,6 +443,8 @@ def test_partition_covers_every_index_exactly_once(kernel_env, n):
                                        (8, 32, "strided", None, 3))]
     variants += [ew.VariantParams(cache="tma", block=b, waves=w, workers=wk)
                  for b, w, wk in ((256, None, None), (64, None, 2), (1024, 2, None))]
+    variants += [ew.VariantParams(unroll=u, block=b, waves=1, workers=wk, prefetch=True)
+                 for u, b, wk in ((1, 256, None), (4, 64, 3), (2, 128, 1))]
     for v in variants:
         for op in ("g[i] += 1", "g[i] = g[i] + 1; if (i < 0) g[0] = 9"):
             guard.fill(0)

@@ -40,15 +40,21 @@ caches = ("tma",) if "--tma-only" in sys.argv else \
 rows = []
 for name in [o for o in ops if o in only]:
     op = ops[name]
-    for u, b, w, c in itertools.product((1, 2, 4), (128, 256, 512, 1024), (0, 1, 2, 4), caches):
+    prefetches = (False, True) if "--prefetch" in sys.argv else (False,)
+    for u, b, w, c, pf in itertools.product((1, 2, 4), (128, 256, 512, 1024), (0, 1, 2, 4),
+                                            caches, prefetches):
+        if pf and w == 0:
+            continue              # one step per thread: nothing to prefetch
         try:
             k = ew.ElementwiseKernel("double a, double *x, double *z", op, "k_" + name,
-                                     ew.VariantParams(unroll=u, block=b, waves=w, cache=c))
+                                     ew.VariantParams(unroll=u, block=b, waves=w, cache=c,
+                                                      prefetch=pf))
         except Exception as exc:  # noqa: BLE001
             print(name, u, b, w, c, "build failed", str(exc)[:200], file=sys.stderr)
             continue
         ms = mean_ms(lambda: k(0.5, x, z))
         rows.append({"op": name, "unroll": u, "block": b, "waves": w, "cache": c,
+                     "prefetch": pf,
                      "GB/s": round(16 * n / ms / 1e6)})
     best = sorted((r for r in rows if r["op"] == name), key=lambda r: -r["GB/s"])[:5]
     for r in best:
