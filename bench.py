@@ -554,12 +554,16 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
     zd = pool.alloc_uninitialized(nd.float64, (n,))
     sig, op = ("double a, double *x, double *z",
                "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
-    t = at.tune_elementwise(sig, op, "polysin", n, axes, args=[0.5, xd, zd],
+    # long statements: the software-pipelined loop keeps loads in flight
+    ps_axes = dict(axes, waves=(0, 1, 2, 4), prefetch=(False, True))
+    t = at.tune_elementwise(sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
+                            constraints=(lambda a: not a["prefetch"] or a["waves"] > 0,),
                             protocol=proto, store=store, burst=10)
     ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**t.best_assignment))
     record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n, t,
            bound="instruction issue + HBM: ~67 instructions/element (~21 FP64); ncu: issue "
-                 "slots 68% busy, FP64 pipe 44%, DRAM 68.5% (profiles/r01_ncu_full_polysin_*)")
+                 "slots 68% busy, FP64 pipe 44%, DRAM 68.5% (profiles/r01_ncu_full_polysin_*); "
+                 "the prefetch variant keeps the next chunk's loads in flight")
     # C3 end to end through the public API: pinned host x -> HBM, kernel, HBM ->
     # pinned host z (16 B/element cross the host link), against the reference's
     # CPU kernel on all host cores -- the compute-heavy case where the GPU wins
