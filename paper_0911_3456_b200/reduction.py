@@ -117,6 +117,7 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
     b["map_tparams"] = b.pop("op_tparams")
     b["map_params"] = b.pop("op_params")
     b.update(name=name, unroll=variant.unroll, block=variant.block,
+             prefetch=variant.prefetch, no_prefetch=not variant.prefetch,
              preamble=_preamble_text(preamble), chunking=_CHUNK_TOKEN[variant.chunking],
              acc_t=spec.acc_dtype.cname, out_t=spec.out_dtype.cname,
              neutral=spec.neutral, reduce_expr=spec.reduce_expr, map_expr=spec.mapped)

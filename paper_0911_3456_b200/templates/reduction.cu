@@ -136,6 +136,29 @@ ${unpack}
     };
     rtcg::for_each<1>(sp.lo + sp.first, tl.head_hi, sp.step, elem);
     rtcg::for_each<1>(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
+{% if prefetch %}
+    // software pipeline (prefetch=True): the next step's chunks are loaded
+    // before this step's map/fold runs
+    long c = tl.c_lo + sp.first;
+${vec_decls_next}
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const long cu = c + u * sp.step;
+        if (cu < tl.c_hi) {
+${vec_loads_next}
+        }
+    }
+    for (; c < tl.c_hi; c += U * sp.step) {
+${vec_decls}
+${vec_copy_next}
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long cu = c + (U + u) * sp.step;
+            if (cu < tl.c_hi) {
+${vec_loads_next}
+            }
+        }
+{% endif %}{% if no_prefetch %}
     for (long c = tl.c_lo + sp.first; c < tl.c_hi; c += U * sp.step) {
 ${vec_decls}
 #pragma unroll
@@ -145,6 +168,7 @@ ${vec_decls}
 ${vec_loads}
             }
         }
+{% endif %}
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const long cu = c + u * sp.step;

@@ -257,3 +257,27 @@ def test_threads_sharing_a_kernel_get_their_own_results(kernel_env):
         return all(int(k(arrays[t])) == want[t] for _ in range(50))
     with ThreadPoolExecutor(8) as ex:
         assert all(ex.map(worker, range(8)))
+
+
+@pytest.mark.parametrize("unroll,block,waves", [(1, 256, 1), (2, 128, 2), (4, 64, 1)])
+def test_prefetch_pipeline_is_bit_identical(kernel_env, unroll, block, waves):
+    """prefetch=True only moves loads earlier: each thread folds the same
+    chunks in the same order, so results are bitwise those of the plain loop
+    (float dot, a transcendental map, wrapping int64 sum)."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(44)
+    n = 2_000_003
+    hx = rng.uniform(-2, 2, n).astype(np.float32)
+    hy = rng.uniform(-2, 2, n).astype(np.float32)
+    hi = rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64)
+    x, y = nd.from_host(pool, nd.float32, hx), nd.from_host(pool, nd.float32, hy)
+    xi = nd.from_host(pool, nd.int64, hi)
+    got = {}
+    for pf in (False, True):
+        v = ew.VariantParams(unroll=unroll, block=block, waves=waves, prefetch=pf)
+        got[pf] = (rd.dot_kernel(nd.float32, v, **kwargs)(x, y),
+                   rd.make_reduction("float *x", nd.float64, "0", "a + b", "sin(x[i])",
+                                     "sumsin", v, **kwargs)(x),
+                   rd.sum_kernel(nd.int64, v, **kwargs)(xi))
+    assert [g.tobytes() for g in got[True]] == [g.tobytes() for g in got[False]]
+    assert int(got[True][2]) == int(hi.sum())
