@@ -26,7 +26,8 @@ for n in (1, 5, 37, 1000, 65_539):
     z = pool.alloc(nd.float32, (n + 1,))
     for v in (ew.VariantParams(), ew.VariantParams(unroll=4, block=64, waves=1,
                                                   chunking="contiguous-blocks"),
-              ew.VariantParams(unroll=16, block=1024, waves=2)):
+              ew.VariantParams(unroll=16, block=1024, waves=2),
+              ew.VariantParams(unroll=2, block=64, workers=3, prefetch=True)):
         ew.ElementwiseKernel("float a, float *x, float b, float *y, float *z",
                              "z[i] = a * x[i] + b * y[i]", "axpy", v)(2.0, x, -3.0, y, z, n=n)
         ew.ElementwiseKernel("float *x, float *z", "z[i] = x[i + 1] - x[i]", "nb", v)(x, z, n=n)
@@ -34,7 +35,8 @@ for n in (1, 5, 37, 1000, 65_539):
         ew.ElementwiseKernel("float *x, float *z", "z[i] = 2 * x[i]", "al", v)(x, x, n=n)
         for cache in ("default", "tma"):
             rv = ew.VariantParams(unroll=v.unroll, block=max(64, v.block), waves=v.waves,
-                                  chunking=v.chunking, cache=cache)
+                                  chunking=v.chunking, cache=cache, workers=v.workers,
+                                  prefetch=v.prefetch)
             float(rd.dot_kernel(nd.float32, rv)(x, y, n=n))
             float(rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i+1] - x[i]",
                                     name="tv", variant=rv)(x, n=n))
