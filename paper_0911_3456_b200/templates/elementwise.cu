@@ -162,8 +162,7 @@ ${smem_loads}
                     rtcg_op<${lane_types}>(cu * E + k${lane_args});
 ${vec_stores}
             }
-            __syncwarp();
-            if (lane_id == 0) rtcg::tma::mbar_arrive(rtcg_empty + s);
+            rtcg::tma::release_stage(rtcg_empty + s);
         }
     }
 }

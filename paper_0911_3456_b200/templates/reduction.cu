@@ -107,8 +107,7 @@ ${smem_loads}
                     for (int k = 0; k < E; ++k)
                         acc = rtcg_fold(acc, rtcg_map<${lane_types}>(t * TE + cu * E + k${lane_args}));
                 }
-                __syncwarp();
-                if (lane_id == 0) rtcg::tma::mbar_arrive(rtcg_empty + s);
+                rtcg::tma::release_stage(rtcg_empty + s);
             }
         }
     }

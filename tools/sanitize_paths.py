@@ -52,8 +52,8 @@ for n in (1, 37, 20_000, 100_003):
     a = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n))
     b8 = nd.from_host(pool, nd.int8, rng.integers(-9, 9, n).astype(np.int8))
     c = pool.alloc(nd.float64, (n,))
-    for blk in (64, 256, 1024):
-        tv = ew.VariantParams(cache="tma", block=blk)
+    for blk, wk in ((64, None), (256, None), (1024, None), (128, 2)):   # workers=2: ring wraps
+        tv = ew.VariantParams(cache="tma", block=blk, workers=wk)
         ew.ElementwiseKernel("double *x, double *z", "z[i] = x[i] * 2 + sin(x[i])", "tps", tv)(a, c)
         ew.ElementwiseKernel("double *x, double *z", "z[i] += x[i]", "trw", tv)(a, c)
         ew.ElementwiseKernel("int8_t *b, double *x, double *z", "z[i] = b[i] * x[i]", "tmx",
