@@ -489,7 +489,7 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
     proto = at.MeasurementProtocol(warmup=1, repeats=3)
     store = at.TuneStore()
 
-    def best_ms(fn, reps=3, burst=10):
+    def best_ms(fn, reps=5, burst=10):
         """Per-launch time as the headline measures it: the mean of a burst of
         back-to-back launches between two events (best of ``reps`` bursts)."""
         fn()
