@@ -291,3 +291,12 @@ def test_algorithmic_bytes_follow_the_access_analysis():
     assert at.algorithmic_bytes(dot, x, y) == 8_000
     peak, kind = at.measured_hbm_gbs()
     assert peak > 1000 and kind in ("measured", "fallback")
+
+
+def test_default_axes_add_prefetch_for_calls():
+    assert "prefetch" not in at.default_axes("z[i] = a * x[i] + b * y[i]")
+    assert "prefetch" not in at.default_axes("z[i] = (float) x[i] * 2")
+    assert at.default_axes("z[i] = sin(x[i]) + 1")["prefetch"] == (False, True)
+    assert at.default_axes("fabsf(x[i])")["prefetch"] == (False, True)
+    assert at._check_axes(None, "exp(x[i])")["prefetch"] == (False, True)
+    assert "prefetch" not in at._check_axes({"unroll": (1,)}, "exp(x[i])")
