@@ -43,6 +43,7 @@ N_PER_GPU = 1 << 28
 METRIC = "Elementwise/reduction GB/s vs B200 HBM peak at 1/2/4/8 GPU; speedup vs CPU ref"
 WORKLOAD = "ReductionKernel dot sum(x*y) float32 n=2^28 per GPU, autotuned block/unroll"
 FALLBACK_HBM = 6650.0
+NOMINAL_HBM = 7672.0   # HBM3e spec: 3996 MHz x 2 transfers x 7680-bit bus / 8 (GB/s)
 
 
 def _env_int(name, default):
@@ -436,6 +437,8 @@ def run_ours(args) -> int:
                      "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
                      if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "nominal_peak": NOMINAL_HBM,
+                     "frac_of_nominal": round(achieved / NOMINAL_HBM, 4),
                      "traffic": _ncu_traffic("dot_k"),
                      "kernel": kernel.launch_config(gx, gy)["entry"],
                      "algorithmic_bytes_per_launch": algo_bytes,
