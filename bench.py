@@ -504,7 +504,9 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
         return best
 
     def record(name, fn, nbytes, tuned, **extra):
-        ms = best_ms(fn)
+        with ClockSampler(rt.current_device()) as clk:
+            ms = best_ms(fn)
+        extra = dict(extra, clocks=clk.summary())
         gbs = nbytes / (ms * 1e-3) / 1e9
         out[name] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
                      "algorithmic_bytes": nbytes, "variant": tuned.best_assignment,
