@@ -111,6 +111,15 @@ int rtcg_function_set_max_dynamic_smem(rtcg_function_t function, int bytes);
 int rtcg_launch(rtcg_function_t function, unsigned grid, unsigned block,
                 unsigned dynamic_smem, rtcg_stream_t stream, void **params);
 
+/* rtcg_launch with launch flags.  RTCG_LAUNCH_OVERLAP_PREVIOUS: programmatic
+ * dependent launch -- the kernel may start while the previous kernel on the
+ * stream drains, up to its first `griddepcontrol.wait`; the caller asserts the
+ * previous kernel writes nothing this one reads before that point (the
+ * reduction templates wait before touching their scratch). */
+#define RTCG_LAUNCH_OVERLAP_PREVIOUS 1u
+int rtcg_launch_ex(rtcg_function_t function, unsigned grid, unsigned block,
+                   unsigned dynamic_smem, rtcg_stream_t stream, void **params, unsigned flags);
+
 /* --- device memory (replaces src/ndarray.py:158-160, :216, :316-336) ----- */
 int rtcg_mem_alloc(uint64_t nbytes, uint64_t *dptr);
 int rtcg_mem_free(uint64_t dptr);

@@ -126,6 +126,8 @@ _PROTOTYPES = {
     "rtcg_function_set_max_dynamic_smem": (_vp, _int),
     "rtcg_launch": (_vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _vp,
                     ctypes.POINTER(_vp)),
+    "rtcg_launch_ex": (_vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _vp,
+                       ctypes.POINTER(_vp), ctypes.c_uint),
     "rtcg_mem_alloc": (_u64, ctypes.POINTER(_u64)),
     "rtcg_mem_free": (_u64,),
     "rtcg_mem_alloc_async": (_u64, _vp, ctypes.POINTER(_u64)),
@@ -209,7 +211,7 @@ def fastlaunch():
             raise RuntimeMissing(
                 f"_fastlaunch is not built ({exc}); run `python -m paper_0911_3456_b200._build`"
             ) from exc
-        mod.set_launcher(ctypes.cast(lib().rtcg_launch, ctypes.c_void_p).value)
+        mod.set_launcher(ctypes.cast(lib().rtcg_launch_ex, ctypes.c_void_p).value)
         _fast = mod
     return _fast
 
@@ -488,6 +490,14 @@ def launch(function: int, grid: int, block: int, params, smem: int = 0,
     s = current_stream() if stream is None else getattr(stream, "handle", stream)
     _check(lib().rtcg_launch(function, grid, block, smem, s or None, params),
            "launch")
+
+
+def launch_overlapped(function: int, grid: int, block: int, params, smem: int = 0,
+                      stream: int | None = None) -> None:
+    """Programmatic dependent launch (see rtcg_launch_ex in the header)."""
+    s = current_stream() if stream is None else getattr(stream, "handle", stream)
+    _check(lib().rtcg_launch_ex(function, grid, block, smem, s or None, params, 1),
+           "launch (overlapped)")
 
 
 # --- memory ------------------------------------------------------------------------------

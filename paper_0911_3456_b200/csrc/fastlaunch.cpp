@@ -20,7 +20,7 @@
 namespace {
 
 using launch_fn = int (*)(void *function, unsigned grid, unsigned block, unsigned smem,
-                          void *stream, void **params);
+                          void *stream, void **params, unsigned flags);   // rtcg_launch_ex
 launch_fn g_launch = nullptr;
 
 PyObject *s_dtype, *s_size, *s_freed, *s_block, *s_address;
@@ -146,14 +146,21 @@ struct VecUse {
     bool written;
 };
 
-// plan.launch(args, n, base, stream, max_grid, extra) -> grid (int), 0 when
+// plan.launch(args, n, base, stream, max_grid, extra[, flags]) -> grid (int), 0 when
 // n == 0 (nothing launched), None = take the Python path, -status on a launch
 // error.  `extra` holds the trailing uint64 parameters (reductions);
-// `max_grid` >= 0 caps the grid (a reduction's partials capacity), -1 = none.
+// `max_grid` >= 0 caps the grid (a reduction's partials capacity), -1 = none;
+// `flags` are rtcg_launch_ex flags (RTCG_LAUNCH_OVERLAP_PREVIOUS).
 PyObject *plan_launch(Plan *self, PyObject *const *argv, Py_ssize_t argc) {
-    if (argc != 6) {
-        PyErr_SetString(PyExc_TypeError, "launch(args, n, base, stream, max_grid, extra)");
+    if (argc != 6 && argc != 7) {
+        PyErr_SetString(PyExc_TypeError,
+                        "launch(args, n, base, stream, max_grid, extra[, flags])");
         return nullptr;
+    }
+    unsigned flags = 0;
+    if (argc == 7) {
+        flags = static_cast<unsigned>(PyLong_AsUnsignedLong(argv[6]));
+        if (PyErr_Occurred()) return nullptr;
     }
     PyObject *args = argv[0];
     if (!PyTuple_Check(args)) Py_RETURN_NONE;
@@ -264,14 +271,14 @@ PyObject *plan_launch(Plan *self, PyObject *const *argv, Py_ssize_t argc) {
         return nullptr;
     }
     const int status = g_launch(e.fn, static_cast<unsigned>(grid), self->block, e.smem,
-                                reinterpret_cast<void *>(stream), ptrs);
+                                reinterpret_cast<void *>(stream), ptrs, flags);
     if (status != 0) return PyLong_FromLong(-status);   // the caller raises the runtime error
     return PyLong_FromLongLong(grid);
 }
 
 PyMethodDef plan_methods[] = {
     {"launch", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)()>(plan_launch)),
-     METH_FASTCALL, "launch(args, n, base, stream, max_grid, extra) -> grid | None"},
+     METH_FASTCALL, "launch(args, n, base, stream, max_grid, extra[, flags]) -> grid | None"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyTypeObject PlanType = {PyVarObject_HEAD_INIT(nullptr, 0)};
@@ -284,7 +291,7 @@ PyObject *set_launcher(PyObject *, PyObject *arg) {
 }
 
 PyMethodDef module_methods[] = {
-    {"set_launcher", set_launcher, METH_O, "address of rtcg_launch in librtcg_b200.so"},
+    {"set_launcher", set_launcher, METH_O, "address of rtcg_launch_ex in librtcg_b200.so"},
     {nullptr, nullptr, 0, nullptr}};
 
 PyModuleDef module_def = {PyModuleDef_HEAD_INIT, "_fastlaunch",

@@ -112,6 +112,7 @@ struct Driver {
     X(cuGraphLaunch, CUresult(CUgraphExec, CUstream))                        \
     X(cuGraphExecDestroy, CUresult(CUgraphExec))                             \
     X(cuGraphDestroy, CUresult(CUgraph))                                     \
+    X(cuLaunchKernelEx, CUresult(const CUlaunchConfig *, CUfunction, void **, void **)) \
     X(cuIpcGetMemHandle, CUresult(CUipcMemHandle *, CUdeviceptr))            \
     X(cuIpcOpenMemHandle_v2, CUresult(CUdeviceptr *, CUipcMemHandle, unsigned)) \
     X(cuIpcCloseMemHandle, CUresult(CUdeviceptr))                            \
@@ -497,6 +498,32 @@ int rtcg_launch(rtcg_function_t function, unsigned grid, unsigned block, unsigne
     CU_CALL(g_drv.cuLaunchKernel(reinterpret_cast<CUfunction>(function), grid, 1, 1, block, 1, 1,
                                  dynamic_smem, reinterpret_cast<CUstream>(stream), params, nullptr),
             "cuLaunchKernel");
+    return RTCG_OK;
+}
+
+int rtcg_launch_ex(rtcg_function_t function, unsigned grid, unsigned block,
+                   unsigned dynamic_smem, rtcg_stream_t stream, void **params, unsigned flags) {
+    if (!(flags & RTCG_LAUNCH_OVERLAP_PREVIOUS))
+        return rtcg_launch(function, grid, block, dynamic_smem, stream, params);
+    if (!function || grid == 0 || block == 0)
+        return fail(RTCG_ERR_INVALID, "rtcg_launch_ex: grid=%u block=%u", grid, block);
+    NEED_CONTEXT();
+    CUlaunchAttribute attr;
+    memset(&attr, 0, sizeof(attr));
+    attr.id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    attr.value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDimX = grid;
+    cfg.gridDimY = cfg.gridDimZ = 1;
+    cfg.blockDimX = block;
+    cfg.blockDimY = cfg.blockDimZ = 1;
+    cfg.sharedMemBytes = dynamic_smem;
+    cfg.hStream = reinterpret_cast<CUstream>(stream);
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CU_CALL(g_drv.cuLaunchKernelEx(&cfg, reinterpret_cast<CUfunction>(function), params, nullptr),
+            "cuLaunchKernelEx");
     return RTCG_OK;
 }
 

@@ -314,7 +314,7 @@ def p2p_capable(group=None) -> bool:
 
 
 def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
-                   collective: str = "auto"):
+                   collective: str = "auto", overlap_previous: bool = False):
     """Global reduction of a ReductionKernel over sharded arguments.
 
     ``"p2p"`` -- one launch per GPU: the local two-stage reduction and the
@@ -330,6 +330,10 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
     ``"auto"`` -- p2p when every rank has its own peer-accessible GPU, else
     allreduce when exact, else allgather.  Everything runs in stream order on
     torch's current stream; p2p and allgather give identical bits.
+    ``overlap_previous`` (p2p only) lets this rank's reduction start while the
+    previous kernel on the stream drains -- see ``ReductionKernel.launch``;
+    with the exchange inside the kernel this also hides the previous step's
+    exchange latency.
     """
     import torch
     import torch.distributed as dist
@@ -351,7 +355,8 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
         with _runtime.use_stream(stream):
             first = next(a for a in local_args if isinstance(a, nd.NdArray))
             out = first.pool.alloc_uninitialized(spec.out_dtype, ())
-            kernel.launch(*local_args, n=n_local, base=base, out=out, peers=mailbox)
+            kernel.launch(*local_args, n=n_local, base=base, out=out, peers=mailbox,
+                          overlap_previous=overlap_previous)
             if return_device:
                 return out
             value = out.to_host()

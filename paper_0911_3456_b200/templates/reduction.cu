@@ -27,6 +27,7 @@ ${name}_g(${kparams_generic}, const long start, const long end,
     ${acc_t} *rtcg_partials, ${acc_t} *rtcg_result, ${out_t} *rtcg_out,
     unsigned int *rtcg_ticket, const rtcg::xr *rtcg_xr, const unsigned long long rtcg_epoch)
 {
+    asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
     ${acc_t} acc = ${neutral};
     const rtcg::span sp = rtcg::partition<rtcg::${chunking}>(start, end);
@@ -49,6 +50,7 @@ ${name}(${kparams_vector}, const long start, const long end,
     ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
     const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
 {
+    asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
     constexpr int E = ${width};
     constexpr int U = 1;
@@ -124,6 +126,7 @@ ${name}(${kparams_vector}, const long start, const long end,
     ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
     const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
 {
+    asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
     constexpr int E = ${width};
     constexpr int U = ${unroll};

@@ -23,8 +23,10 @@ uint64_t rec_vals[128];
 uint64_t rec_fn, rec_stream;
 unsigned rec_grid, rec_block, rec_smem;
 int rec_count, rec_calls;
-int record(void *fn, unsigned grid, unsigned block, unsigned smem, void *stream, void **params) {
-    rec_fn = (uint64_t)fn; rec_grid = grid; rec_block = block; rec_smem = smem;
+unsigned rec_flags;
+int record(void *fn, unsigned grid, unsigned block, unsigned smem, void *stream, void **params,
+           unsigned flags) {
+    rec_fn = (uint64_t)fn; rec_grid = grid; rec_block = block; rec_smem = smem; rec_flags = flags;
     rec_stream = (uint64_t)stream; rec_calls++;
     for (int k = 0; k < rec_count; ++k) memcpy(&rec_vals[k], params[k], 8);
     return 0;
@@ -46,7 +48,7 @@ def fl(tmp_path_factory):
     _fastlaunch.set_launcher(ctypes.cast(rec.record, ctypes.c_void_p).value)
     yield _fastlaunch, rec
     # restore the real launcher: plans cached by other tests call it directly
-    _fastlaunch.set_launcher(ctypes.cast(_runtime.lib().rtcg_launch, ctypes.c_void_p).value)
+    _fastlaunch.set_launcher(ctypes.cast(_runtime.lib().rtcg_launch_ex, ctypes.c_void_p).value)
 
 
 @pytest.fixture()
@@ -163,6 +165,9 @@ def test_declined_calls_and_limits(fl, pool):
     assert calls.value == before
     ctypes.c_int.in_dll(rec, "rec_count").value = 7
     assert plan.launch((1.0, x, z), None, 0, 0, -1, (11, 22)) == 1
+    assert ctypes.c_uint.in_dll(rec, "rec_flags").value == 0
+    assert plan.launch((1.0, x, z), None, 0, 0, -1, (11, 22), 1) == 1
+    assert ctypes.c_uint.in_dll(rec, "rec_flags").value == 1
     vals = list((ctypes.c_uint64 * 7).in_dll(rec, "rec_vals"))
     assert vals[3:] == [0, 64, 11, 22]
     assert np.float64(1.0).view(np.uint64) == vals[0]

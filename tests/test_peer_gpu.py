@@ -240,3 +240,31 @@ def test_missing_peer_times_out_softly(pool):
     assert int(k(x)) == int(np.arange(1000).sum())                          # context alive
     for m in group:
         m.close()
+
+
+def test_overlapped_launches_with_the_peer_exchange(pool):
+    """Emulated ranks launching back-to-back overlapped reductions: each
+    rank's next reduction streams while its previous one exchanges."""
+    from paper_0911_3456_b200 import ndarray as nd, reduction as rd
+    rng = np.random.default_rng(61)
+    x = rng.uniform(-1, 1, 2_000_011).astype(np.float32)
+    y = rng.uniform(-1, 1, 2_000_011).astype(np.float32)
+    world = 3
+    dot = rd.dot_kernel(nd.float32)
+    shards = _shard(pool, nd.float32, [x, y], world)
+    want = par.ordered_fold(lambda a, b: a + b, 0.0, _rank_accumulators(dot, shards))
+    from paper_0911_3456_b200 import _runtime as rt
+    group = par.PeerMailbox.local_group(world)
+    streams = [rt.Stream() for _ in range(world)]
+    outs = [[pool.alloc_uninitialized(nd.float64, ()) for _ in range(world)] for _ in range(8)]
+    for j in range(8):
+        for r in range(world):
+            with rt.use_stream(streams[r].handle):
+                s = dot.launch(*shards[r][0], base=shards[r][1], peers=group[r],
+                               overlap_previous=True)
+                rt.memcpy_dtod(outs[j][r].address, s.result, 8)
+    for st in streams:
+        st.synchronize()
+    assert all(float(o.get()) == float(want) for row in outs for o in row)
+    for m in group:
+        m.close()

@@ -283,3 +283,32 @@ def test_prefetch_pipeline_is_bit_identical(kernel_env, unroll, block, workers):
                    rd.sum_kernel(nd.int64, v, **kwargs)(xi))
     assert [g.tobytes() for g in got[True]] == [g.tobytes() for g in got[False]]
     assert int(got[True][2]) == int(hi.sum())
+
+
+def test_overlapped_launches_give_the_same_results(kernel_env):
+    """overlap_previous=True (programmatic dependent launch): consecutive
+    reductions sharing one scratch, on the same and on different inputs,
+    each produce exactly the result of an ordinary launch."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(51)
+    n = 3_000_017
+    hx = rng.uniform(-1, 1, n).astype(np.float32)
+    hy = rng.uniform(-1, 1, n).astype(np.float32)
+    x, y = nd.from_host(pool, nd.float32, hx), nd.from_host(pool, nd.float32, hy)
+    dot = rd.dot_kernel(nd.float32, ew.VariantParams(waves=1), **kwargs)
+    sq = rd.make_reduction("float *x", nd.float32, "0", "a + b", "x[i] * x[i]", "sq_ov",
+                           ew.VariantParams(waves=2), **kwargs)
+    want = (float(dot(x, y)), float(sq(x)), float(sq(y)))
+    outs = [pool.alloc_uninitialized(nd.float32, ()) for _ in range(90)]
+    for j in range(30):
+        dot.launch(x, y, out=outs[3 * j], overlap_previous=True)
+        sq.launch(x, out=outs[3 * j + 1], overlap_previous=True)
+        sq.launch(y, out=outs[3 * j + 2], overlap_previous=True)
+    got = [float(o.get()) for o in outs]
+    assert got == list(want) * 30
+    ints = nd.from_host(pool, nd.int64, rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64))
+    s = rd.sum_kernel(nd.int64, **kwargs)
+    o = pool.alloc_uninitialized(nd.int64, ())
+    for _ in range(20):
+        s.launch(ints, out=o, overlap_previous=True)
+    assert int(o.get()) == int(s(ints))
