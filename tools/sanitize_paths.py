@@ -80,6 +80,14 @@ for st in streams:
 assert all(int(ks._read(ks.scratch(0, st.handle).result, nd.int64)) == int(xs.sum())
            for st in streams)
 checks += 9 if EXCHANGE else 0
+# overlapped (programmatic dependent) reductions back to back
+ov = rd.dot_kernel(nd.float32)
+oo = pool.alloc(nd.float32, ())
+big_x = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, 200_003).astype(np.float32))
+for _ in range(6):
+    ov.launch(big_x, big_x, out=oo, overlap_previous=True)
+assert abs(float(oo.get()) - float(ov(big_x, big_x))) == 0
+checks += 6
 # streamed host call
 hx = rng.uniform(-1, 1, 300_001).astype(np.float32)
 hz = np.zeros_like(hx)
