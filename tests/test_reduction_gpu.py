@@ -307,8 +307,15 @@ def test_overlapped_launches_give_the_same_results(kernel_env):
     got = [float(o.get()) for o in outs]
     assert got == list(want) * 30
     ints = nd.from_host(pool, nd.int64, rng.integers(-(1 << 62), 1 << 62, n, dtype=np.int64))
-    s = rd.sum_kernel(nd.int64, **kwargs)
-    o = pool.alloc_uninitialized(nd.int64, ())
-    for _ in range(20):
-        s.launch(ints, out=o, overlap_previous=True)
-    assert int(o.get()) == int(s(ints))
+    for v in (ew.VariantParams(), ew.VariantParams(cache="tma", block=256, workers=5)):
+        s = rd.sum_kernel(nd.int64, v, **kwargs)
+        o = pool.alloc_uninitialized(nd.int64, ())
+        for _ in range(20):
+            s.launch(ints, out=o, overlap_previous=True)
+        assert int(o.get()) == int(s(ints))
+    general = rd.make_reduction("float *x", nd.float64, "0", "a + b", "x[i] * (double) (i & 3)",
+                                "gen_ov", **kwargs)                       # uses i: general path
+    og = pool.alloc_uninitialized(nd.float64, ())
+    for _ in range(10):
+        general.launch(x, out=og, overlap_previous=True)
+    assert float(og.get()) == float(general(x))
