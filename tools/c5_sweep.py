@@ -158,6 +158,13 @@ def main():
             rec("chain_sum_two_pass", chain_then_sum, 2 * sz * n)
             rec("chain_sum_fused", lambda: fr(x, y).free(), 2 * sz * n)
             rec("sum", lambda: sm.launch(x, out=o), sz * n)
+            # back-to-back overlapped reductions (programmatic dependent launch):
+            # mean of a 20-launch burst, as a stream of reductions would run
+            def sum_burst():
+                for _ in range(20):
+                    sm.launch(x, out=o, overlap_previous=True)
+            ms = dev_ms(sum_burst) / 20
+            res["sum_overlapped"] = {"us": round(ms * 1e3, 2), "GB/s": round(sz * n / ms / 1e6, 1)}
             rec("max", lambda: mx.launch(x, out=o), sz * n)
             rec("dot", lambda: dot.launch(x, y, out=o), 2 * sz * n)
             row[dname] = res
