@@ -545,7 +545,8 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
         t = at.tune_reduction(spec, name, big, axes, args=[xf], protocol=proto,
                               store=store, burst=3)
         k = rd.ReductionKernel(spec, name, ew.VariantParams(**t.best_assignment))
-        record(f"{name}_f32_2p32", lambda: k.launch(xf, out=o32), 4 * big, t,
+        record(f"{name}_f32_2p32", lambda: k.launch(xf, out=o32, overlap_previous=True),
+               4 * big, t,
                note="L2 norm = sqrt(sumsq) on the host" if name == "sumsq" else "max|x|")
     xf.free()
     xi = pool.alloc_uninitialized(nd.int64, (big,))
@@ -556,7 +557,7 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
     t = at.tune_reduction(spec, "sum_k", big, axes, args=[xi], protocol=proto,
                           store=store, burst=3)
     si = rd.ReductionKernel(spec, "sum_k", ew.VariantParams(**t.best_assignment))
-    record("sum_i64_2p32", lambda: si.launch(xi, out=o64), 8 * big, t,
+    record("sum_i64_2p32", lambda: si.launch(xi, out=o64, overlap_previous=True), 8 * big, t,
            note="values in [-2^62, 2^62): the sum wraps (bit-exact, order independent)")
     xi.free()
 
