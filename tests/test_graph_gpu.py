@@ -63,3 +63,32 @@ def test_captured_chain_replays_like_eager_calls(pool, shared_cache):
 def test_capture_rejects_legacy_stream():
     with pytest.raises(ValueError):
         graph.Graph(_runtime.Stream(handle=0))
+
+
+def test_captured_overlapped_reductions(pool, shared_cache):
+    """Overlapped (programmatic dependent) reduction launches inside a CUDA
+    graph: captured as programmatic edges, replays give the eager results."""
+    n = 1 << 20
+    rng = np.random.default_rng(9)
+    hx = rng.uniform(-1, 1, n).astype(np.float32)
+    x = nd.from_host(pool, nd.float32, hx)
+    outs = [pool.alloc(nd.float32, ()) for _ in range(3)]
+    dot = rd.dot_kernel(nd.float32, cache=shared_cache)
+    sq = rd.make_reduction("float *x", nd.float32, "0", "a > b ? a : b", "x[i] * x[i]",
+                           "mx_g", cache=shared_cache)
+    want = (float(dot(x, x)), float(sq(x)))
+    g = graph.Graph()
+    with _runtime.use_stream(g.stream):
+        dot.launch(x, x, out=outs[0])
+        sq.launch(x, out=outs[1])
+        g.synchronize()
+    with g.capture():
+        dot.launch(x, x, out=outs[0], overlap_previous=True)
+        sq.launch(x, out=outs[1], overlap_previous=True)
+        dot.launch(x, x, out=outs[2], overlap_previous=True)
+    for o in outs:
+        o.copy_from_host(np.zeros((), np.float32))
+    for _ in range(20):
+        g.launch()
+    g.synchronize()
+    assert [float(o.get()) for o in outs] == [want[0], want[1], want[0]]
