@@ -336,8 +336,10 @@ class ReductionKernel:
         reduction of a loop) is still folding, and wait for it only before
         touching the shared scratch (``griddepcontrol.wait`` in
         ``rtcg::finish``).  The caller asserts that the previous kernel on
-        the stream writes nothing this call reads (its inputs).  Measured on
-        B200: back-to-back dot f32 at 2^24 / 2^26 / 2^28 +19 / +5 / +2 %."""
+        the stream writes nothing this call reads (its inputs).  With
+        ``peers``, one GPU per rank is assumed (ranks emulated on one GPU
+        share its SMs with each other's waiting grids).  Measured on B200:
+        back-to-back dot f32 at 2^24 / 2^26 / 2^28 +19 / +5 / +2 %."""
         if stream is not None:
             stream = getattr(stream, "handle", stream)
         if peers is None:

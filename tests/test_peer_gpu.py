@@ -244,13 +244,20 @@ def test_missing_peer_times_out_softly(pool):
 
 def test_overlapped_launches_with_the_peer_exchange(pool):
     """Emulated ranks launching back-to-back overlapped reductions: each
-    rank's next reduction streams while its previous one exchanges."""
-    from paper_0911_3456_b200 import ndarray as nd, reduction as rd
+    rank's next reduction streams while its previous one exchanges.
+
+    Emulated ranks share one GPU's SMs: an overlapped grid that launched
+    early holds its CTAs while it waits, so many queued grids of several
+    ranks could starve a rank that has not exchanged yet.  With one GPU per
+    rank that cannot happen (a rank's waiting grid only waits on its own
+    predecessor, resident by construction); here the grids are pinned to 2
+    CTAs so every queued grid fits on the device at once."""
+    from paper_0911_3456_b200 import elementwise as ew, ndarray as nd, reduction as rd
     rng = np.random.default_rng(61)
     x = rng.uniform(-1, 1, 2_000_011).astype(np.float32)
     y = rng.uniform(-1, 1, 2_000_011).astype(np.float32)
     world = 3
-    dot = rd.dot_kernel(nd.float32)
+    dot = rd.dot_kernel(nd.float32, ew.VariantParams(workers=2))
     shards = _shard(pool, nd.float32, [x, y], world)
     want = par.ordered_fold(lambda a, b: a + b, 0.0, _rank_accumulators(dot, shards))
     from paper_0911_3456_b200 import _runtime as rt

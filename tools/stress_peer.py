@@ -17,8 +17,12 @@ x = rng.integers(-1000, 1000, 1_000_003).astype(np.int64)
 bounds = [r * x.size // world for r in range(world + 1)]
 shards = [(nd.from_host(pool, nd.int64, x[bounds[r]:bounds[r + 1]]), bounds[r])
           for r in range(world)]
-kernels = [rd.sum_kernel(nd.int64), rd.max_kernel(nd.int64),
-           rd.make_reduction("int64_t *x", nd.int64, "0", "a + b", "x[i] * x[i]", "sq")]
+# emulated ranks share the SMs: pin grids small and drain every 16 epochs so
+# overlapped grids waiting on their predecessors can never fill the device
+# (with one GPU per rank a waiting grid only waits on its own predecessor)
+v = ew.VariantParams(workers=2)
+kernels = [rd.sum_kernel(nd.int64, v), rd.max_kernel(nd.int64, v),
+           rd.make_reduction("int64_t *x", nd.int64, "0", "a + b", "x[i] * x[i]", "sq", v)]
 wants = [int(x.sum()), int(x.max()), int((x * x).sum())]
 spin = ew.ElementwiseKernel("long iters, float *w", "float a = w[i]; for (long t = 0; "
                             "t < iters; ++t) a = a * 0.999f + 0.001f; w[i] = a", "spin")
@@ -35,6 +39,9 @@ for j in range(epochs):
             s = k.launch(shards[r][0], base=shards[r][1], peers=group[r],
                          overlap_previous=bool(rng.random() < 0.7))
             rt.memcpy_dtod(outs[j][r].address, s.result, 8)
+    if j % 16 == 15:
+        for st in streams:
+            st.synchronize()
 for st in streams:
     st.synchronize()
 for m in group:
