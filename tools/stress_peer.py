@@ -27,6 +27,13 @@ wants = [int(x.sum()), int(x.max()), int((x * x).sum())]
 spin = ew.ElementwiseKernel("long iters, float *w", "float a = w[i]; for (long t = 0; "
                             "t < iters; ++t) a = a * 0.999f + 0.001f; w[i] = a", "spin")
 busy = [pool.alloc(nd.float32, (2048,)) for _ in range(world)]
+# load every module before any rank waits on the device: in one process a
+# module load can wait for running kernels, i.e. for a rank spinning in its
+# exchange (with one GPU per rank that is a stall, here it would deadlock)
+spin(1, busy[0])
+for k in kernels:
+    k(shards[0][0])
+rt.synchronize()
 group = par.PeerMailbox.local_group(world)
 streams = [rt.Stream() for _ in range(world)]
 outs = [[pool.alloc_uninitialized(nd.int64, ()) for _ in range(world)] for _ in range(epochs)]
