@@ -155,12 +155,12 @@ _NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
 XR_MAX = 64                             # rtcg::XR_MAX in templates/prelude.cuh
 XR_ERROR = 3 * XR_MAX                   # rtcg::XR_ERROR: epoch of a timed-out wait
 MAILBOX_BYTES = 8 * (3 * XR_MAX + 8)    # epoch flags, two accumulator banks, error word
+_XR = struct.Struct(f"<ii{XR_MAX}Q")     # struct rtcg::xr {int rank, world; u64 mbox[64];}
 
 
 class PeerTimeout(RuntimeError):
     """A peer never published its accumulator (the kernel gave up after 20 s
     and returned its local value)."""
-_XR = struct.Struct(f"<ii{XR_MAX}Q")     # struct rtcg::xr {int rank, world; u64 mbox[64];}
 
 
 class PeerMailbox:
