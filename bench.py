@@ -457,7 +457,7 @@ def run_ours(args) -> int:
                         + " (numpy scalar)",
                 "streamed_value": None if streamed_s is None else
                 round(8 * total_n / streamed_s / 1e9, 2),
-                "streamed_path": "ReductionKernel(driver.In(x), driver.In(y)): 32 MiB chunks, "
+                "streamed_path": "ReductionKernel(driver.In(x), driver.In(y)): 64 MiB chunks, "
                                  "uploads overlapped with per-chunk reductions",
                 "link_h2d_gbs": round(link_gbs, 2),
                 "link_frac": round(e2e_gbs / (link_gbs * d.world), 4),
@@ -603,7 +603,7 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
         "value": round(16 * n / str_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
         "d2h_bytes_per_step": 8 * n, "steps": 3,
         "path": "ElementwiseKernel(0.5, driver.In(x), driver.Out(z)) on pinned host arrays: "
-                "32 MiB chunks, upload / kernel / download overlapped on two streams",
+                "64 MiB chunks, upload / kernel / download overlapped on two streams",
         "sequential_value": round(16 * n / seq_s / 1e9, 2),
         "sequential_path": "GPUArray.copy_from_host + ElementwiseKernel + GPUArray.to_host"}
     try:

@@ -415,7 +415,7 @@ class ReductionKernel:
         return {"entry": handle.name, "grid": grid, "block": self.variant.block, "n": n,
                 "smem": smem}
 
-    HOST_CHUNK_BYTES = 32 << 20
+    HOST_CHUNK_BYTES = 64 << 20
 
     def _call_host(self, args, n, base: int, want_device: bool, chunk: int | None = None):
         """Reduction over host arrays (``driver.In``): chunk j's uploads and
