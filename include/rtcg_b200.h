@@ -86,6 +86,10 @@ void rtcg_free_buffer(void *p);
 int rtcg_init(void);
 int rtcg_device_count(int *count);
 int rtcg_device_info_get(int device, rtcg_device_info *info);
+/* "dddd:bb:dd.f" of a visible device (cuDeviceGetPCIBusId): a process-
+ * independent identity (ordinals depend on CUDA_VISIBLE_DEVICES), used to
+ * decide whether ranks really run on distinct, peer-reachable GPUs. */
+int rtcg_device_pci_bus_id(int device, char *buf, int len);
 /* Retain the device's primary context (shared with the CUDA runtime / torch)
  * and make it current on the calling thread. */
 int rtcg_set_device(int device);
@@ -162,6 +166,9 @@ int rtcg_stream_synchronize(rtcg_stream_t stream);
 int rtcg_event_create(rtcg_event_t *event);
 int rtcg_event_destroy(rtcg_event_t event);
 int rtcg_event_record(rtcg_event_t event, rtcg_stream_t stream);
+/* Work submitted to `stream` after this call waits for `event` (cuStreamWaitEvent);
+ * streamed host calls order their private streams after the caller's stream. */
+int rtcg_stream_wait_event(rtcg_stream_t stream, rtcg_event_t event);
 int rtcg_event_synchronize(rtcg_event_t event);
 int rtcg_event_elapsed_ms(rtcg_event_t start, rtcg_event_t end, float *ms);
 

@@ -149,6 +149,8 @@ _PROTOTYPES = {
     "rtcg_event_create": (ctypes.POINTER(_vp),),
     "rtcg_event_destroy": (_vp,),
     "rtcg_event_record": (_vp, _vp),
+    "rtcg_device_pci_bus_id": (_int, ctypes.c_char_p, _int),
+    "rtcg_stream_wait_event": (_vp, _vp),
     "rtcg_event_synchronize": (_vp,),
     "rtcg_event_elapsed_ms": (_vp, _vp, ctypes.POINTER(ctypes.c_float)),
     "rtcg_stream_begin_capture": (_vp,),
@@ -295,6 +297,13 @@ def device_info(device: int | None = None) -> dict:
     return out
 
 
+def pci_bus_id(device: int) -> str:
+    """Process-independent identity of a visible device ("0000:1b:00.0")."""
+    buf = ctypes.create_string_buffer(32)
+    _check(lib().rtcg_device_pci_bus_id(device, buf, len(buf)), "pci bus id")
+    return buf.value.decode().lower()
+
+
 def set_device(device: int) -> None:
     """Make ``device``'s primary context current on this thread."""
     if getattr(_tls, "device", None) == device:
@@ -341,6 +350,10 @@ class Stream:
 
     def synchronize(self) -> None:
         _check(lib().rtcg_stream_synchronize(self.handle or None), "stream sync")
+
+    def wait(self, event: "Event") -> None:
+        """Order work submitted to this stream after ``event``."""
+        stream_wait_event(self.handle, event)
 
     def close(self) -> None:
         if self._owned and self.handle:
@@ -405,6 +418,32 @@ class Event:
                 _lib.rtcg_event_destroy(handle)
             except Exception:  # pragma: no cover - interpreter shutdown
                 pass
+
+
+def stream_wait_event(stream, event: Event) -> None:
+    """Work submitted to ``stream`` (raw handle, 0 = legacy) after this call
+    waits for ``event`` (cuStreamWaitEvent)."""
+    _check(lib().rtcg_stream_wait_event(stream or None, event.handle), "stream wait event")
+
+
+def order_after_current(streams) -> None:
+    """Make every stream in ``streams`` wait for the work already submitted
+    to this thread's current stream (one event, recorded now)."""
+    ev = _order_event()
+    ev.record(current_stream())
+    for st in streams:
+        stream_wait_event(getattr(st, "handle", st), ev)
+
+
+def _order_event() -> Event:
+    dev = current_device()
+    evs = getattr(_tls, "order_events", None)
+    if evs is None:
+        evs = _tls.order_events = {}
+    ev = evs.get(dev)
+    if ev is None:
+        ev = evs[dev] = Event()
+    return ev
 
 
 # --- graphs ------------------------------------------------------------------------------

@@ -100,6 +100,7 @@ struct Driver {
     X(cuStreamCreate, CUresult(CUstream *, unsigned))                      \
     X(cuStreamDestroy_v2, CUresult(CUstream))                              \
     X(cuStreamSynchronize, CUresult(CUstream))                             \
+    X(cuStreamWaitEvent, CUresult(CUstream, CUevent, unsigned))            \
     X(cuEventCreate, CUresult(CUevent *, unsigned))                        \
     X(cuEventDestroy_v2, CUresult(CUevent))                                \
     X(cuEventRecord, CUresult(CUevent, CUstream))                          \
@@ -117,6 +118,7 @@ struct Driver {
     X(cuIpcOpenMemHandle_v2, CUresult(CUdeviceptr *, CUipcMemHandle, unsigned)) \
     X(cuIpcCloseMemHandle, CUresult(CUdeviceptr))                            \
     X(cuDeviceCanAccessPeer, CUresult(int *, CUdevice, CUdevice))            \
+    X(cuDeviceGetPCIBusId, CUresult(char *, int, CUdevice))                  \
     X(cuGetErrorString, CUresult(CUresult, const char **))
 #define RTCG_DECLARE(name, sig) fnptr<sig> name = nullptr;
     RTCG_DRIVER_FNS(RTCG_DECLARE)
@@ -383,6 +385,16 @@ int rtcg_device_info_get(int device, rtcg_device_info *info) {
     CU_CALL(g_drv.cuDeviceTotalMem_v2(&total, dev), "cuDeviceTotalMem");
     info->total_mem = total;
     CU_CALL(g_drv.cuDriverGetVersion(&info->driver_version), "cuDriverGetVersion");
+    return RTCG_OK;
+}
+
+int rtcg_device_pci_bus_id(int device, char *buf, int len) {
+    int s = driver_ready();
+    if (s != RTCG_OK) return s;
+    if (!buf || len < 13) return fail(RTCG_ERR_INVALID, "bus id buffer needs >= 13 bytes");
+    CUdevice dev;
+    CU_CALL(g_drv.cuDeviceGet(&dev, device), "cuDeviceGet");
+    CU_CALL(g_drv.cuDeviceGetPCIBusId(buf, len, dev), "cuDeviceGetPCIBusId");
     return RTCG_OK;
 }
 
@@ -921,6 +933,14 @@ int rtcg_event_record(rtcg_event_t event, rtcg_stream_t stream) {
     NEED_CONTEXT();
     CU_CALL(g_drv.cuEventRecord(reinterpret_cast<CUevent>(event), reinterpret_cast<CUstream>(stream)),
             "cuEventRecord");
+    return RTCG_OK;
+}
+
+int rtcg_stream_wait_event(rtcg_stream_t stream, rtcg_event_t event) {
+    NEED_CONTEXT();
+    CU_CALL(g_drv.cuStreamWaitEvent(reinterpret_cast<CUstream>(stream),
+                                    reinterpret_cast<CUevent>(event), 0),
+            "cuStreamWaitEvent");
     return RTCG_OK;
 }
 

@@ -38,7 +38,7 @@ from . import ndarray as nd
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
            "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op", "PeerMailbox",
-           "PeerTimeout", "peer_mailbox"]
+           "PeerTimeout", "peer_mailbox", "p2p_capable", "peer_plan"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -155,12 +155,14 @@ _NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
 XR_MAX = 64                             # rtcg::XR_MAX in templates/prelude.cuh
 XR_ERROR = 3 * XR_MAX                   # rtcg::XR_ERROR: epoch of a timed-out wait
 MAILBOX_BYTES = 8 * (3 * XR_MAX + 8)    # epoch flags, two accumulator banks, error word
-_XR = struct.Struct(f"<ii{XR_MAX}Q")     # struct rtcg::xr {int rank, world; u64 mbox[64];}
+_XR = struct.Struct(f"<ii{XR_MAX}QQ")    # struct rtcg::xr {int rank, world; u64 mbox[64], timeout_ns;}
+DEFAULT_TIMEOUT_S = 20.0
 
 
 class PeerTimeout(RuntimeError):
-    """A peer never published its accumulator (the kernel gave up after 20 s
-    and returned its local value)."""
+    """A peer never published its accumulator (the kernel gave up after the
+    mailbox's timeout and poisoned result/out: all bits set, i.e. NaN for
+    floats and -1 / MAX for integers)."""
 
 
 class PeerMailbox:
@@ -173,7 +175,8 @@ class PeerMailbox:
     at a time (calls on one mailbox are serialised by the stream).  Not
     capturable in CUDA graphs (the epoch is a launch parameter)."""
 
-    def __init__(self, rank: int, world: int, addresses, *, owned=(), opened=()) -> None:
+    def __init__(self, rank: int, world: int, addresses, *, owned=(), opened=(),
+                 timeout_s: float = DEFAULT_TIMEOUT_S) -> None:
         if not 1 <= world <= XR_MAX:
             raise ValueError(f"world size must be in [1, {XR_MAX}], got {world}")
         if len(addresses) != world or not 0 <= rank < world:
@@ -183,7 +186,11 @@ class PeerMailbox:
         self._owned, self._opened = list(owned), list(opened)
         self._epoch = 0
         self._lock = threading.Lock()
-        blob = _XR.pack(rank, world, *self.addresses, *([0] * (XR_MAX - world)))
+        if not timeout_s > 0:
+            raise ValueError("timeout_s must be positive")
+        self.timeout_s = float(timeout_s)
+        blob = _XR.pack(rank, world, *self.addresses, *([0] * (XR_MAX - world)),
+                        int(self.timeout_s * 1e9))
         self.descriptor = _runtime.mem_alloc(len(blob))
         self._owned.append(self.descriptor)
         host = ctypes.create_string_buffer(blob, len(blob))
@@ -196,14 +203,18 @@ class PeerMailbox:
             return self._epoch
 
     def check(self, stream=None) -> None:
-        """Synchronise ``stream`` and raise :class:`PeerTimeout` if any
-        exchange on this mailbox timed out waiting for a peer."""
+        """Synchronise ``stream`` and raise :class:`PeerTimeout` if an
+        exchange on this mailbox timed out waiting for a peer since the last
+        check.  The error word is cleared when it is reported, so a later
+        healthy exchange checks clean."""
         word = ctypes.c_uint64()
         st = 0 if stream is None else getattr(stream, "handle", stream)
-        _runtime.memcpy_dtoh(ctypes.addressof(word), self.addresses[self.rank] + 8 * XR_ERROR,
-                             8, st)
+        err = self.addresses[self.rank] + 8 * XR_ERROR
+        _runtime.memcpy_dtoh(ctypes.addressof(word), err, 8, st)
         _runtime.stream_synchronize(st)
         if word.value:
+            _runtime.memset_async(err, 0, 8, st)
+            _runtime.stream_synchronize(st)
             raise PeerTimeout(f"rank {self.rank}: the peer exchange of epoch {word.value} "
                               f"timed out waiting for another rank")
 
@@ -215,7 +226,7 @@ class PeerMailbox:
         return box
 
     @classmethod
-    def create(cls, group=None) -> "PeerMailbox":
+    def create(cls, group=None, timeout_s: float = DEFAULT_TIMEOUT_S) -> "PeerMailbox":
         """Collective over a torch.distributed group (one process per GPU):
         allocate and zero this rank's mailbox, exchange CUDA IPC handles
         (``all_gather_object``, which also orders every zeroing before any
@@ -246,17 +257,17 @@ class PeerMailbox:
             _runtime.mem_free(box)
             raise RuntimeError(f"peer mailboxes unavailable on ranks "
                                f"{[r for r, ok in enumerate(verdicts) if not ok]}: {error}")
-        mb = cls(rank, world, addresses, owned=[box], opened=opened)
+        mb = cls(rank, world, addresses, owned=[box], opened=opened, timeout_s=timeout_s)
         mb.devices = tuple(d for d, _ in everyone)
         return mb
 
     @classmethod
-    def local_group(cls, world: int) -> list["PeerMailbox"]:
+    def local_group(cls, world: int, timeout_s: float = DEFAULT_TIMEOUT_S) -> list["PeerMailbox"]:
         """``world`` mailboxes on the current device, one per emulated rank
         (single-process tests of the exchange protocol: launch rank r on its
         own stream with ``peers=group[r]``)."""
         boxes = [cls._new_box() for _ in range(world)]
-        group = [cls(r, world, boxes) for r in range(world)]
+        group = [cls(r, world, boxes, timeout_s=timeout_s) for r in range(world)]
         group[0]._owned.extend(boxes)
         return group
 
@@ -296,19 +307,41 @@ def peer_mailbox(group=None, stream: int = 0) -> PeerMailbox:
     return mb
 
 
+def peer_plan(bus_ids, visible) -> bool:
+    """Whether ranks on the devices ``bus_ids`` (one PCI bus id per rank) can
+    exchange through peer memory, seen from one process whose visible devices
+    are ``visible`` ({bus id: local ordinal}).  Ranks must sit on distinct
+    physical GPUs (bus ids, not ordinals: under per-rank CUDA_VISIBLE_DEVICES
+    every rank calls its GPU device 0), and every peer's GPU must be visible
+    here -- CUDA IPC cannot map memory of a device this process cannot see."""
+    if len(set(bus_ids)) != len(bus_ids):
+        return False
+    return all(b in visible for b in bus_ids)
+
+
 def p2p_capable(group=None) -> bool:
-    """True when every rank runs on its own device and all pairs have peer
-    access (NVLink / NVSwitch on an HGX B200).  Ranks that share a device
-    (test setups) take the NCCL path under ``collective="auto"``."""
+    """True when every rank runs on its own device, each rank sees the other
+    ranks' devices, and all pairs have peer access (NVLink / NVSwitch on an
+    HGX B200).  Decided on PCI bus ids gathered from every rank, and agreed
+    collectively.  Ranks that share a device (test setups) take the NCCL path
+    under ``collective="auto"``."""
     import torch.distributed as dist
     g = _group_object(group)
     for owner, ok in _capable.get(id(g), ()):
         if owner is g:
             return ok
-    devices = [None] * dist.get_world_size(group)
-    dist.all_gather_object(devices, _runtime.current_device(), group=group)
-    ok = len(set(devices)) == len(devices) and all(
-        _runtime.can_access_peer(a, b) for a in devices for b in devices)
+    world = dist.get_world_size(group)
+    mine = _runtime.pci_bus_id(_runtime.current_device())
+    bus_ids = [None] * world
+    dist.all_gather_object(bus_ids, mine, group=group)
+    visible = {_runtime.pci_bus_id(d): d for d in range(_runtime.device_count())}
+    ok = peer_plan(bus_ids, visible)
+    if ok:
+        me = visible[mine]
+        ok = all(visible[b] == me or _runtime.can_access_peer(me, visible[b]) for b in bus_ids)
+    verdicts = [None] * world          # every rank takes the same path
+    dist.all_gather_object(verdicts, ok, group=group)
+    ok = all(verdicts)
     _capable.setdefault(id(g), []).append((g, ok))
     return ok
 

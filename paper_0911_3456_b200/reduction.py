@@ -127,22 +127,28 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
 class _Scratch:
     """Per-device partials / result / out / ticket buffers of one kernel."""
 
-    def __init__(self, acc_size: int, out_size: int) -> None:
+    def __init__(self, acc_size: int, out_size: int, stream: int = 0) -> None:
         self.capacity = 0
         self.partials = 0
         self.acc_size, self.out_size = acc_size, out_size
+        self.stream = stream
         self.result = _runtime.mem_alloc(64)
         self.out = self.result + 16
         self.ticket = self.result + 32
-        _runtime.memset_async(self.result, 0, 64)
+        # zeroed on the stream the scratch is keyed by, so the first launch
+        # there is ordered after the ticket reset (cuMemAlloc is not zeroed)
+        _runtime.memset_async(self.result, 0, 64, stream)
 
     def ensure(self, count: int) -> None:
         if count > self.capacity:
-            if self.partials:
-                _runtime.synchronize()
-                _runtime.mem_free(self.partials)
             cap = max(count, 2048)
-            self.partials = _runtime.mem_alloc(cap * self.acc_size)
+            if self.partials:
+                # stream-ordered retirement: the old buffer is released after
+                # the launches already queued on this scratch's stream (no
+                # device-wide synchronisation, which would block on peers'
+                # exchange kernels spinning on the same GPU)
+                _runtime.mem_free_async(self.partials, self.stream)
+            self.partials = _runtime.mem_alloc_async(cap * self.acc_size, self.stream)
             self.capacity = cap
 
 
@@ -240,7 +246,7 @@ class ReductionKernel:
             s = self._scratch.get(key)
             if s is None:
                 s = self._scratch[key] = _Scratch(self.spec.acc_dtype.size,
-                                                 self.spec.out_dtype.size)
+                                                 self.spec.out_dtype.size, key[1])
             return s
 
     def _pick(self, vectors, n):
@@ -458,6 +464,8 @@ class ReductionKernel:
         staging = [[pool.alloc_uninitialized(p.dtype, (step,)) if isinstance(a, HostArg)
                     else None for p, a in zip(params, args)] for _ in streams]
         acc_size = self.spec.acc_dtype.size
+        _runtime.order_after_current(streams)   # see ElementwiseKernel._call_host
+        done = False
         try:
             for j in range(count):
                 lo, hi = j * step, min(total, (j + 1) * step)
@@ -478,6 +486,7 @@ class ReductionKernel:
                     _runtime.memcpy_dtod(accs.address + j * acc_size, s.result, acc_size)
             for st in streams:
                 st.synchronize()
+            done = True
             s = self.scratch(dev)
             s.ensure(1)
             self._launch_combine(accs.address, count, s.result, out.address)
@@ -487,6 +496,9 @@ class ReductionKernel:
             out.free()
             return value
         finally:
+            if not done:       # drain in-flight copies before the staging is reused
+                for st in streams:
+                    st.synchronize()
             accs.free()
             for stage in staging:
                 for buf in stage:

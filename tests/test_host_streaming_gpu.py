@@ -119,3 +119,56 @@ def test_reduction_over_host_inputs(kernel_env, pinned):
     assert int(s(drv.In(ints[:0]))) == 0                 # empty: the neutral
     with pytest.raises(ValueError):
         s(drv.Out(np.zeros(4, np.int64)))
+
+
+def _slow_producer(kwargs):
+    """Writes y[i] = i % 13 after a long dependent sinf chain per element, so
+    the kernel is still running when the host call is issued."""
+    return ew.make_elementwise(
+        "float *y, int reps",
+        "float v = 0.0f; for (int k = 0; k < reps; ++k) v = sinf(v + 1.0f); "
+        "y[i] = (float) (i % 13) + (v > 10.0f ? 1.0f : 0.0f)", "slow_producer", **kwargs)
+
+
+@pytest.mark.parametrize("user_stream", [False, True])
+def test_streamed_call_waits_for_producer_on_callers_stream(kernel_env, user_stream):
+    """the streamed call's private streams must start after the
+    work already queued on the caller's stream (here: the kernel writing the
+    device argument y)."""
+    from paper_0911_3456_b200 import _runtime
+    kwargs, pool = kernel_env
+    n = 1 << 22
+    x = np.arange(n, dtype=np.float32)
+    z = np.zeros(n, np.float32)
+    y = pool.alloc_uninitialized(nd.float32, (n,))
+    prod = _slow_producer(kwargs)
+    add = ew.make_elementwise("float *x, float *y, float *z", "z[i] = x[i] + y[i]",
+                              "add_host", **kwargs)
+    st = _runtime.Stream() if user_stream else None
+    with _runtime.use_stream(st):
+        prod(y, 3000)
+        add(drv.In(x), y, drv.Out(z))
+    want = x + (np.arange(n) % 13).astype(np.float32)
+    assert np.array_equal(z, want)
+    if st is not None:
+        st.synchronize()
+        st.close()
+    y.free()
+
+
+def test_streamed_reduction_waits_for_producer(kernel_env):
+    from paper_0911_3456_b200 import _runtime
+    from paper_0911_3456_b200 import reduction as rd
+    kwargs, pool = kernel_env
+    n = 1 << 22
+    x = np.ones(n, np.int64)
+    y = pool.alloc_uninitialized(nd.float32, (n,))
+    prod = _slow_producer(kwargs)
+    k = rd.make_reduction("int64_t *x, float *y", nd.int64, "0", "a + b",
+                          "x[i] * (int64_t) y[i]", "dot_host_order", **kwargs)
+    st = _runtime.Stream()
+    with _runtime.use_stream(st):
+        prod(y, 3000)
+        got = k(drv.In(x), y)
+    assert int(got) == int((np.arange(n) % 13).sum())
+    st.close()

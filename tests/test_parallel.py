@@ -226,3 +226,19 @@ def test_two_ranks_sharing_the_gpu_reduce_like_one(tmp_path):
             csem.float_reduction_bound(terms, "float32")
         assert got["elementwise_ok"]
     assert results[0] == results[1]           # every rank holds the same answer
+
+
+def test_peer_plan_uses_bus_ids_not_ordinals():
+    """under per-rank CUDA_VISIBLE_DEVICES every rank calls its
+    GPU device 0; distinct physical GPUs must still be recognised (and peers
+    this process cannot see make the exchange impossible)."""
+    a, b = "0000:1b:00.0", "0000:43:00.0"
+    assert par.peer_plan([a, b], {a: 0, b: 1})
+    assert not par.peer_plan([a, a], {a: 0})                 # two ranks, one GPU
+    assert not par.peer_plan([a, b], {a: 0})                 # peer not visible here
+    assert par.peer_plan([a], {a: 0})
+
+
+def test_mailbox_descriptor_layout_matches_the_kernel_struct():
+    # struct rtcg::xr {int rank, world; u64 mbox[64]; u64 timeout_ns;}
+    assert par._XR.size == 8 + 8 * par.XR_MAX + 8
