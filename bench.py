@@ -6,21 +6,32 @@ Headline workload (BASELINE.json configs[1]): ``ReductionKernel`` dot product
 ``sum(x*y)``, float32, n = 2^28 elements per GPU (weak scaling), block/unroll
 autotuned before the timed region.  One step = one full reduction of the
 resident inputs (per-CTA folds + in-kernel ordered combine; for N > 1 also the
-NCCL all-gather of the per-rank partials and the rank-ordered combine).
-``value`` = algorithmic bytes (8 B/element: x and y read once) of all ranks /
-max-over-ranks device time.  Inputs (2 x 1 GiB per GPU) exceed the 126 MB L2,
-so no flush is needed between steps.
+exchange of the per-rank accumulators -- in-kernel over NVLink peer memory, or
+the NCCL baseline -- and the rank-ordered combine).  ``value`` = algorithmic
+bytes (8 B/element: x and y read once) of all ranks / max-over-ranks device
+time.  Inputs (2 x 1 GiB per GPU) exceed the 126 MB L2, so no flush is needed
+between steps.
+
+``--gpus N`` without a launcher (no WORLD_SIZE in the environment) spawns the N
+ranks itself (one process per GPU, RANK/LOCAL_RANK/WORLD_SIZE set, rendezvous
+on 127.0.0.1); under torchrun the launcher's ranks are used.  Ranks that share
+a GPU (more ranks than visible GPUs) use gloo for the plumbing and the NCCL-
+free allreduce/allgather combine; ranks on distinct GPUs use NCCL and the
+in-kernel peer exchange.
 
 The JSON line also carries: ``e2e`` (same metric through the public API with
-pinned host inputs copied in and the scalar read back every step),
-``roofline`` (dominant kernel vs MEASURED_PEAKS.json HBM copy bandwidth),
-``cpu_baseline`` (the reference's CPU kernel on this host, bounded sample),
-``clocks`` (NVML during the timed region) and ``workloads`` (the other
-configs measured the same way: axpy, f64 poly+sin, max|x|, L2, int64 sum).
+pinned host inputs copied in and the scalar read back every step; at N > 1
+each rank uploads its own slice), ``roofline`` (dominant kernel vs
+MEASURED_PEAKS.json HBM copy bandwidth, with the isolated-launch time next to
+the pipelined step time), ``cpu_baseline`` (the reference's own CPU kernel on
+this host, on the same 2^28 arrays), ``clocks`` (NVML during the timed
+region), ``parity`` (flat per-workload checks against exact references) and
+``workloads`` (the other configs: strong-scaled dot, C4 max|x| / L2 / int64
+sum at 2^32 total sharded over the ranks, axpy, f64 poly+sin, the C5 sweep).
 
-``--impl reference`` times the reference's own CPU implementation of the same
-workload (``oracle/_ref``: C emitted by rtcg-kit's generator, compiled with its
-command line, driven with its threading) on all host cores of rank 0.
+``--impl reference`` times the reference's own CPU implementation
+(``baseline/_ref``: the unmodified rtcg-kit, stock ``reduction.dot_kernel``;
+else ``oracle/_ref``) on all host cores of rank 0, on the same arrays.
 """
 
 from __future__ import annotations
@@ -29,9 +40,13 @@ import argparse
 import json
 import math
 import os
+import socket
+import subprocess
 import sys
+import tempfile
 import threading
 import time
+from fractions import Fraction
 from pathlib import Path
 
 import numpy as np
@@ -40,10 +55,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_PER_GPU = 1 << 28
+N_C4 = 1 << 32
 METRIC = "Elementwise/reduction GB/s vs B200 HBM peak at 1/2/4/8 GPU; speedup vs CPU ref"
 WORKLOAD = "ReductionKernel dot sum(x*y) float32 n=2^28 per GPU, autotuned block/unroll"
 FALLBACK_HBM = 6650.0
-NOMINAL_HBM = 7672.0   # HBM3e spec: 3996 MHz x 2 transfers x 7680-bit bus / 8 (GB/s)
+# ncu's DRAM peak for this B200 (dram__bytes.sum.peak_sustained x DRAM clock):
+# 7.13 TB/s read in profiles/r01_ncu_full_dot_k_* is reported as 87.12 % of it
+NCU_DRAM_PEAK = 8184.0
 
 
 def _env_int(name, default):
@@ -61,11 +79,31 @@ def _peaks():
     return FALLBACK_HBM, "fallback"
 
 
+def workload_config(n_gpus: int) -> dict:
+    """The workload identity both arms report (same keys, same values)."""
+    return {"workload": WORKLOAD, "n_per_gpu": N_PER_GPU, "n_total": N_PER_GPU * n_gpus,
+            "inputs": "x, y ~ U(-1,1) float32, numpy default_rng([0, rank])"}
+
+
+def host_inputs(rank: int, n: int = N_PER_GPU, pinned=None):
+    """This rank's slice of the headline inputs (identical in both arms)."""
+    rng = np.random.default_rng([0, rank])
+    if pinned is None:
+        x = rng.uniform(-1, 1, n).astype(np.float32)
+        y = rng.uniform(-1, 1, n).astype(np.float32)
+        return x, y
+    x, y = pinned((n,)), pinned((n,))
+    x[:] = rng.uniform(-1, 1, n).astype(np.float32)
+    y[:] = rng.uniform(-1, 1, n).astype(np.float32)
+    return x, y
+
+
 # --- clocks ------------------------------------------------------------------------------------
 
 
 class ClockSampler:
-    """NVML samples of SM clock and throttle reasons while running."""
+    """NVML samples of SM clock and throttle reasons while running (the GPU
+    is found by PCI bus id, so CUDA_VISIBLE_DEVICES renumbering is harmless)."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -73,7 +111,7 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, device: int, period: float = 0.02) -> None:
+    def __init__(self, bus_id: str | None, period: float = 0.02) -> None:
         self.samples, self.reasons = [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -82,7 +120,8 @@ class ClockSampler:
             import pynvml
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self._h = pynvml.nvmlDeviceGetHandleByPciBusId(bus_id) if bus_id else \
+                pynvml.nvmlDeviceGetHandleByIndex(0)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception as exc:  # pragma: no cover - no NVML
             self._nv = None
@@ -123,108 +162,271 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-# --- distributed plumbing ------------------------------------------------------------------------
+# --- rank spawning and distributed plumbing ------------------------------------------------------
+
+
+def _free_port() -> int:
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        return sock.getsockname()[1]
+
+
+def spawn_env(base: dict, rank: int, world: int, port: int) -> dict:
+    """Environment of self-spawned rank ``rank`` (what torchrun would set)."""
+    env = dict(base)
+    env.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+               LOCAL_WORLD_SIZE=str(world), GROUP_RANK="0", MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(port), RTCG_BENCH_SPAWNED="1")
+    return env
+
+
+def spawn_ranks(argv: list[str], world: int, timeout: float | None = None,
+                script: str | None = None) -> int:
+    """Run this script (or ``script``) as ``world`` rank processes; relay rank
+    0's JSON line.  Returns the worst exit code (a rank that fails fails the
+    run)."""
+    port = _free_port()
+    procs = []
+    target = script or str(Path(__file__).resolve())
+    for r in range(world):
+        procs.append(subprocess.Popen([sys.executable, target, *argv],
+                                      env=spawn_env(os.environ, r, world, port),
+                                      stdout=subprocess.PIPE if r == 0 else subprocess.DEVNULL))
+    out, _ = procs[0].communicate(timeout=timeout)
+    codes = [procs[0].returncode] + [p.wait(timeout=timeout) for p in procs[1:]]
+    text = out.decode(errors="replace")
+    if text:
+        sys.stdout.write(text)
+        sys.stdout.flush()
+    return max(codes, key=abs)
 
 
 class Dist:
-    def __init__(self, gpus: int) -> None:
+    """Rank identity + process group.  One device per local rank
+    (``LOCAL_RANK % device_count``); NCCL when every rank owns its GPU, gloo
+    when ranks share one (NCCL refuses two ranks on one device)."""
+
+    def __init__(self, gpus: int, device_count: int) -> None:
         self.world = _env_int("WORLD_SIZE", 1)
         self.rank = _env_int("RANK", 0)
         self.local = _env_int("LOCAL_RANK", 0)
-        if self.world != gpus and "WORLD_SIZE" in os.environ:
+        local_world = _env_int("LOCAL_WORLD_SIZE", self.world)
+        if self.world != gpus:
             print(f"warning: --gpus {gpus} but WORLD_SIZE={self.world}", file=sys.stderr)
-        self.torch = None
+        self.device = self.local % max(1, device_count)
+        self.shared_gpu = local_world > max(1, device_count)
+        self.torch = self.dist = None
+        self.backend = None
         # RTCG_BENCH_FORCE_DIST=1 runs the multi-GPU code path (process group,
         # cross-GPU exchange of the accumulators) even at world size 1
         self.forced = os.environ.get("RTCG_BENCH_FORCE_DIST") == "1"
+        import torch
+        self.torch = torch
+        torch.cuda.set_device(self.device)
         if self.world > 1 or self.forced:
             if "MASTER_ADDR" not in os.environ:
-                import socket
-                with socket.socket() as sock:
-                    sock.bind(("127.0.0.1", 0))
-                    port = sock.getsockname()[1]
-                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                os.environ.setdefault("MASTER_PORT", str(port))
-                os.environ.setdefault("RANK", "0")
-                os.environ.setdefault("WORLD_SIZE", "1")
-            import torch
+                os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()),
+                                  RANK="0", WORLD_SIZE="1")
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
-            self.torch, self.dist = torch, dist
+            self.backend = "gloo" if self.shared_gpu else "nccl"
+            kwargs = {} if self.shared_gpu else {"device_id": torch.device("cuda", self.device)}
+            dist.init_process_group(self.backend, **kwargs)
+            self.dist = dist
 
     @property
     def distributed(self) -> bool:
-        return self.torch is not None
+        return self.dist is not None
 
     def barrier(self):
         if self.distributed:
             self.dist.barrier()
 
-    def max(self, value: float) -> float:
+    def _reduce(self, value: float, op) -> float:
         if not self.distributed:
             return value
-        t = self.torch.tensor([value], dtype=self.torch.float64, device="cuda")
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        dev = "cpu" if self.backend == "gloo" else "cuda"
+        t = self.torch.tensor([value], dtype=self.torch.float64, device=dev)
+        self.dist.all_reduce(t, op=op)
         return float(t.item())
+
+    def max(self, value: float) -> float:
+        return self._reduce(value, self.dist.ReduceOp.MAX if self.distributed else None)
+
+    def gather(self, obj) -> list:
+        if not self.distributed:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def bcast(self, obj):
+        if not self.distributed:
+            return obj
+        box = [obj]
+        self.dist.broadcast_object_list(box, src=0)
+        return box[0]
 
     def close(self):
         if self.distributed:
             self.dist.destroy_process_group()
 
 
+# --- exact checkers (not the product: torch on the device, integer arithmetic) ---------------------
+#
+# A float32 value is m * 2^(e-24) with an integer |m| < 2^24 (np/torch frexp).
+# Summing the integer mantissas per exponent is exact in float64 as long as a
+# bucket's running sum stays below 2^53 (chunks of <= 2^28 elements); buckets
+# are carried across chunks in int64 and combined in Python integers, so the
+# total is the exact sum -- what math.fsum computes -- at any n, in seconds.
+
+_EOFF, _EBINS = 160, 320
+
+
+def f32_exact_buckets(values) -> np.ndarray:
+    """Per-exponent integer mantissa sums of a float32 torch tensor (exact)."""
+    import torch
+    total = np.zeros(_EBINS, np.int64)
+    flat = values.reshape(-1)
+    step = 1 << 26
+    for lo in range(0, flat.numel(), step):
+        v = flat[lo:lo + step]
+        m, e = torch.frexp(v)
+        mi = torch.ldexp(m, torch.full_like(e, 24)).to(torch.float64)
+        b = torch.bincount((e + _EOFF).to(torch.int64), weights=mi, minlength=_EBINS)
+        total += b.to(torch.int64).cpu().numpy()
+    return total
+
+
+def buckets_value(buckets) -> Fraction:
+    num = 0
+    for k, s in enumerate(np.asarray(buckets, dtype=np.int64).tolist()):
+        if s:
+            num += int(s) << k
+    return Fraction(num, 1 << (_EOFF + 24))
+
+
+def f32_ulp(value: float) -> float:
+    return float(np.spacing(np.float32(abs(value)))) or float(np.finfo(np.float32).tiny)
+
+
+def reduction_check(got: float, exact: Fraction, n: int, sum_abs: float) -> dict:
+    """The float-reduction rule of SURVEY.md §8c.4 against the exact sum:
+    |got - exact| <= 1/2 ulp_f32(exact) + n * 2^-53 * sum|terms|; also whether
+    got is bit-equal to float32(fsum) (the reference's own result)."""
+    ref64 = float(exact)
+    ref32 = float(np.float32(ref64))
+    bound = 0.5 * f32_ulp(ref64) + n * 2.0 ** -53 * sum_abs
+    err = abs(got - ref64)
+    return {"ok": bool(err <= bound), "bit_equal_f32_fsum": bool(np.float32(got) == np.float32(ref32)),
+            "ulps": round(err / f32_ulp(ref64), 4), "err": err, "bound": bound, "want": ref32}
+
+
+def i64_wrapped_sum(values) -> int:
+    """Exact two's-complement (wrapping) sum of an int64 torch tensor."""
+    import torch
+    flat = values.reshape(-1)
+    total = 0
+    step = 1 << 26
+    for lo in range(0, flat.numel(), step):
+        v = flat[lo:lo + step].to(torch.int64)
+        total += int((v & 0xFFFFFFFF).sum().item()) + (int((v >> 32).sum().item()) << 32)
+    return total
+
+
+def wrap64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= 1 << 63 else v
+
+
 # --- CPU reference ---------------------------------------------------------------------------------
 
 
-def cpu_reference(workload: str, steps: int | None = None, warmup: int = 1,
-                  budget_s: float = 10.0, n_sample: int = 1 << 26):
-    """Time the reference CPU kernel on a bounded sample of the workload.
+def _stock_reference():
+    """The unmodified reference (``baseline/_ref``), when installed."""
+    path = ROOT / "baseline" / "_ref"
+    if not (path / "rtcg" / "reduction.py").exists():
+        return None
+    os.environ.setdefault("RTCG_CACHE_DIR", tempfile.mkdtemp(prefix="rtcg-ref-cache-"))
+    if str(path) not in sys.path:
+        sys.path.insert(0, str(path))
+    import rtcg  # noqa: F401
+    from rtcg import ndarray as rnd, reduction as rrd
+    return rnd, rrd
 
-    ``steps`` given: exactly that many timed calls after ``warmup`` (mean);
-    else calls until ``budget_s`` (>= 3, <= 50; best).  Returns a dict."""
-    from oracle import refdrive
-    fn, kind = refdrive.load(workload)
-    threads = refdrive.host_threads()
-    rng = np.random.default_rng(0)
-    x = rng.uniform(-1, 1, n_sample).astype(np.float32)
-    y = rng.uniform(-1, 1, n_sample).astype(np.float32)
-    for _ in range(max(1, warmup)):
-        fn(x, y, workers=threads)  # page in, thread spin-up
-    times = []
-    if steps is not None:
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            fn(x, y, workers=threads)
-        per_call, stat = (time.perf_counter() - t0) / steps, f"mean of {steps} calls"
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_reference(x: np.ndarray, y: np.ndarray, warmup: int = 1, calls: int = 5) -> dict:
+    """The reference's dot f32 on this host's cores, on the given arrays:
+    ``warmup`` calls, then the best of ``calls`` (BASELINE.md §3 protocol:
+    best-of-5 after one warm-up, ``time.perf_counter`` around one call).
+
+    Stock ``rtcg.reduction.dot_kernel(float32)`` from ``baseline/_ref`` with
+    the reference default variant (unroll 4, workers = cores, contiguous
+    blocks); else the reference-generated C in ``oracle/_ref`` driven with the
+    reference's threading."""
+    n = x.size
+    stock = _stock_reference()
+    if stock is not None:
+        rnd, rrd = stock
+        pool = rnd.MemoryPool()
+        gx, gy = rnd.from_host(pool, rnd.float32, x), rnd.from_host(pool, rnd.float32, y)
+        kernel = rrd.dot_kernel(rnd.float32)
+
+        def call():
+            return kernel(gx, gy)
+        kind, how = "reference", "stock rtcg.reduction.dot_kernel(float32) from baseline/_ref " \
+                                 "(unmodified rtcg-kit), default variant"
+        threads = os.cpu_count() or 1
     else:
-        t_end = time.perf_counter() + budget_s
-        while len(times) < 3 or (time.perf_counter() < t_end and len(times) < 50):
-            t0 = time.perf_counter()
-            fn(x, y, workers=threads)
-            times.append(time.perf_counter() - t0)
-        per_call, stat = min(times), f"best of {len(times)} calls"
-    return {"value": round(8 * n_sample / per_call / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "kind": kind, "seconds_per_call": per_call,
-            "calls": steps if steps is not None else len(times),
-            "sample": f"dot f32 n=2^{int(math.log2(n_sample))} per call (bounded sample of the "
-                      f"2^28 workload), x,y~U(-1,1) seed 0, reference variant unroll=4 "
-                      f"contiguous-blocks, {threads} worker threads, {stat}"}
+        from oracle import refdrive
+        fn, kind = refdrive.load("dot_k")
+        threads = host_threads()
+
+        def call():
+            return fn(x, y, workers=threads)
+        how = f"oracle/_ref dot_k ({kind}), reference variant unroll=4 contiguous-blocks"
+    value = None
+    for _ in range(max(1, warmup)):
+        value = call()
+    times = []
+    for _ in range(max(1, calls)):
+        t0 = time.perf_counter()
+        value = call()
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    if stock is not None:
+        gx.free()
+        gy.free()
+    return {"value": round(8 * n / best / 1e9, 3), "unit": "GB/s", "cores": threads,
+            "kind": kind, "seconds_per_call": best, "result": float(value),
+            "sample": f"dot f32 n=2^{int(math.log2(n))} (the full per-GPU workload, same arrays "
+                      f"as the GPU arm), {how}, {threads} worker threads, best of {len(times)} "
+                      f"calls after {max(1, warmup)} warm-up"}
 
 
 def run_reference(args) -> int:
     """CPU reference arm: rank 0 only, no GPU or process group needed."""
     if _env_int("RANK", 0) != 0:
         return 0
-    base = cpu_reference("dot_k", steps=args.steps, warmup=args.warmup)
+    x, y = host_inputs(0)
+    base = cpu_reference(x, y, warmup=args.warmup, calls=args.steps)
     line = {"impl": "reference", "metric": METRIC, "value": base["value"], "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(base["seconds_per_call"] * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": WORKLOAD + " (CPU: bounded sample)",
-                                            "n": 1 << 26},
+            "data": "synthetic", "config": workload_config(args.gpus),
             "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": base["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "result": base["result"]}
+    line["config"]["note"] = ("CPU arm: rank 0 times one GPU's share (2^28) of the weak-scaled "
+                              "workload; GB/s is size-independent at this size")
     emit(line)
     return 0
 
@@ -232,10 +434,10 @@ def run_reference(args) -> int:
 # --- GPU arm ----------------------------------------------------------------------------------------
 
 
-def _time_steps(rt, step, k: int, per_step: bool = True):
-    """Device time of k steps on the current stream, plus per-step durations
-    (``per_step=False``: only the two bracketing events, so nothing is
-    recorded between back-to-back launches; per-step = the mean)."""
+def _time_steps(rt, step, k: int, per_step: bool = False):
+    """Device time (ms) of k steps on the current stream, plus per-step
+    durations (``per_step=False``: only the two bracketing events, so nothing
+    is recorded between back-to-back launches; per-step = the mean)."""
     if not per_step:
         start, stop = rt.Event(), rt.Event()
         start.record()
@@ -255,341 +457,417 @@ def _time_steps(rt, step, k: int, per_step: bool = True):
     return events[0].elapsed_ms(events[-1]), per
 
 
-def run_ours(args) -> int:
-    d = Dist(args.gpus)
-    from paper_0911_3456_b200 import _runtime as rt
-    from paper_0911_3456_b200 import autotune as at
-    from paper_0911_3456_b200 import ndarray as nd
-    from paper_0911_3456_b200 import parallel as par
-    from paper_0911_3456_b200 import reduction as rd
-    from paper_0911_3456_b200 import elementwise as ew
+class Ctx:
+    """Everything the workloads share."""
 
-    rt.set_device(d.local)
-    info = rt.device_info(d.local)
-    stream_handle = d.torch.cuda.current_stream().cuda_stream if d.distributed else 0
-    pool = nd.MemoryPool(device=d.local)
+    def __init__(self, args, d: Dist) -> None:
+        from paper_0911_3456_b200 import _runtime as rt
+        from paper_0911_3456_b200 import autotune as at
+        from paper_0911_3456_b200 import elementwise as ew
+        from paper_0911_3456_b200 import ndarray as nd
+        from paper_0911_3456_b200 import parallel as par
+        from paper_0911_3456_b200 import reduction as rd
+        self.args, self.d = args, d
+        self.rt, self.at, self.ew, self.nd, self.par, self.rd = rt, at, ew, nd, par, rd
+        self.torch = d.torch
+        rt.set_device(d.device)
+        self.info = rt.device_info(d.device)
+        self.bus_id = rt.pci_bus_id(d.device)
+        self.pool = nd.MemoryPool(device=d.device)
+        self.peak, self.peak_kind = _peaks()
+        self.store = at.TuneStore()
+        self.proto = at.MeasurementProtocol(warmup=1, repeats=3)
+        self.collective = None
+        self.launch_count = 0
+
+    def timed(self, step, k: int, warmup: int = 3, per_step: bool = False, on_start=None):
+        """Warm up, then device-time k steps between barriers; returns
+        (max-over-ranks ms per step, this rank's per-step ms list).
+        ``on_start`` runs right before the first timed step."""
+        d, rt = self.d, self.rt
+        for _ in range(warmup):
+            step()
+        rt.synchronize()
+        d.barrier()
+        rt.synchronize()
+        if on_start is not None:
+            on_start()
+        total, per = _time_steps(rt, step, k, per_step)
+        rt.synchronize()
+        d.barrier()
+        return d.max(total / k), per
+
+    def tune_on_rank0(self, tune):
+        """Tune on rank 0 alone (ranks sharing a GPU would disturb each
+        other's timings) and give every rank the winner."""
+        best = None
+        if self.d.rank == 0:
+            best = tune()
+        self.d.barrier()
+        return self.d.bcast(best)
+
+    def reducer(self, kernel):
+        """Step function of a global reduction of sharded args over the
+        ranks (in-kernel peer exchange, NCCL, or gloo); returns
+        (step(*sharded) -> 0-d out array, launches per step)."""
+        d, par = self.d, self.par
+        if not d.distributed:
+            def step(*args, out):
+                kernel.launch(*[a.local for a in args], out=out, overlap_previous=True)
+            return step, 1
+        coll = self.collective
+
+        def step(*args, out=None):
+            par.sharded_reduce(kernel, *args, return_device=True, collective=coll,
+                               overlap_previous=coll == "p2p").free()
+        return step, 1 if coll == "p2p" else 2
+
+    def global_value(self, kernel, *args):
+        """The reduction's global result as a host scalar (every rank)."""
+        if not self.d.distributed:
+            return kernel(*[a.local for a in args])
+        return self.par.sharded_reduce(kernel, *args, collective=self.collective)
+
+
+def choose_collective(c: Ctx) -> str | None:
+    """p2p (in-kernel exchange over peer memory) when every rank has its own
+    peer-reachable GPU and a trial exchange works on every rank; else "auto"
+    (NCCL allreduce when exact, else allgather + ordered combine)."""
+    d, par = c.d, c.par
+    if not d.distributed:
+        return None
+    wanted = os.environ.get("RTCG_BENCH_COLLECTIVE")
+    if wanted:
+        return wanted
+    if d.shared_gpu or not par.p2p_capable():
+        return "auto"
+    # trial exchange on a tiny input
+    x = c.nd.from_host(c.pool, c.nd.int64, np.arange(1000, dtype=np.int64) + d.rank)
+    sx = par.ShardedArray(x, 1000 * d.rank, 1000 * d.world, d.rank, d.world)
+    k = c.rd.sum_kernel(c.nd.int64)
+    ok = 1.0
+    try:
+        got = par.sharded_reduce(k, sx, collective="p2p")
+        want = sum(int(np.arange(1000).sum()) + 1000 * r for r in range(d.world))
+        ok = 1.0 if int(got) == want else 0.0
+    except Exception as exc:  # noqa: BLE001 - decided collectively
+        print(f"warning: p2p trial failed: {exc}", file=sys.stderr)
+        ok = 0.0
+    x.free()
+    agreed = -c.d.max(-ok)            # min over ranks
+    return "p2p" if agreed > 0 else "auto"
+
+
+def headline_dot(c: Ctx) -> dict:
+    """configs[1]: dot f32, 2^28 per GPU, autotuned; the timed steps."""
+    d, rt, at, ew, nd, par, rd = c.d, c.rt, c.at, c.ew, c.nd, c.par, c.rd
     n = N_PER_GPU
     total_n = n * d.world
-    peak, peak_kind = _peaks()
+    hx, hy = host_inputs(d.rank, n, pinned=lambda s: nd.pinned_empty(s, nd.float32))
+    gx, gy = nd.from_host(c.pool, nd.float32, hx), nd.from_host(c.pool, nd.float32, hy)
+    lo = n * d.rank
+    sx = par.ShardedArray(gx, lo, total_n, d.rank, d.world)
+    sy = par.ShardedArray(gy, lo, total_n, d.rank, d.world)
+    spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
+    out = c.pool.alloc_uninitialized(nd.float32, ())
 
-    with rt.use_stream(stream_handle):
-        # resident inputs: this rank's slice of a global 2^28*N array
-        lo, _ = par.shard_range(total_n, d.rank, d.world)
-        hx = nd.pinned_empty((n,), nd.float32)
-        hy = nd.pinned_empty((n,), nd.float32)
-        rng = np.random.default_rng([0, d.rank])
-        hx[:] = rng.uniform(-1, 1, n).astype(np.float32)
-        hy[:] = rng.uniform(-1, 1, n).astype(np.float32)
-        gx, gy = nd.from_host(pool, nd.float32, hx), nd.from_host(pool, nd.float32, hy)
-        sx = par.ShardedArray(gx, lo, total_n, d.rank, d.world)
-        sy = par.ShardedArray(gy, lo, total_n, d.rank, d.world)
-
-        # autotune block x unroll for (dot, float32, n) -- outside the timed region
-        spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
+    def tune():
         t0 = time.perf_counter()
         # variants ranked as the metric is measured: mean of back-to-back launches
         axes = dict(at.DEFAULT_AXES, waves=(0, 1, 2), cache=("default", "tma"))
         tuned = at.tune_reduction(spec, "dot_k", n, axes, args=[gx, gy],
                                   constraints=(lambda a: a["cache"] != "tma" or a["unroll"] == 1,),
-                                  protocol=at.MeasurementProtocol(warmup=1, repeats=3),
-                                  store=at.TuneStore(), burst=10)
-        out = pool.alloc_uninitialized(nd.float32, ())
-        # confirmation stage: the tuner's top 8 re-timed over 50-launch bursts of
-        # overlapped launches (how the timed steps run)
-        # (its 3 x 10-launch samples leave ~1-2 % of noise in the ranking)
+                                  protocol=c.proto, store=c.store, burst=10)
+        # confirmation: the tuner's top 8 re-timed over 50-launch bursts of
+        # overlapped launches (its 3 x 10-launch samples leave ~1-2 % noise)
         finalists = sorted((e for e in tuned.table if e.status == "ok"),
                            key=lambda e: e.stat_seconds)[:8]
         confirm = []
         for e in finalists:
             k = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**e.as_dict()))
-            run = at.device_timer(lambda k=k: k.launch(gx, gy, out=out,
-                                                       overlap_previous=True), 50)
+            run = at.device_timer(lambda k=k: k.launch(gx, gy, out=out, overlap_previous=True),
+                                  50)
             run()
             confirm.append((min(run() for _ in range(2)), e.as_dict()))
-        best = min(confirm, key=lambda c: c[0])[1] if confirm else tuned.best_assignment
-        if os.environ.get("RTCG_BENCH_DOT_VARIANT"):   # experiments: pin the variant
-            best = json.loads(os.environ["RTCG_BENCH_DOT_VARIANT"])
-        tune_s = time.perf_counter() - t0
-        kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
+        best = min(confirm, key=lambda q: q[0])[1] if confirm else tuned.best_assignment
+        return {"variant": best, "seconds": round(time.perf_counter() - t0, 2),
+                "from_store": tuned.from_store}
+    tuned = c.tune_on_rank0(tune)
+    best = tuned["variant"]
+    if os.environ.get("RTCG_BENCH_DOT_VARIANT"):   # experiments: pin the variant
+        best = json.loads(os.environ["RTCG_BENCH_DOT_VARIANT"])
+    kernel = rd.ReductionKernel(spec, "dot_k", ew.VariantParams(**best))
+    step, per_step_launches = c.reducer(kernel)
 
-        collective = None
-        # steps are back-to-back reductions over inputs nothing writes, so each
-        # may start streaming while the previous one folds (programmatic
-        # dependent launch; ReductionKernel.launch(overlap_previous=True))
-        if not d.distributed:
-            def step():
-                kernel.launch(gx, gy, out=out, overlap_previous=True)
-        else:
-            # the product path: one launch per GPU, accumulators exchanged over
-            # NVLink peer memory inside the kernel; NCCL only when peers are
-            # unreachable (RTCG_BENCH_COLLECTIVE overrides, e.g. "allgather")
-            collective = os.environ.get("RTCG_BENCH_COLLECTIVE") or (
-                "p2p" if par.p2p_capable() else "auto")
+    # parity on this data before timing: exact sum of the float32 products
+    got = float(c.global_value(kernel, sx, sy))
+    tx = c.torch.as_tensor(gx, device="cuda")
+    ty = c.torch.as_tensor(gy, device="cuda")
+    prods = tx * ty                                   # IEEE float32 products (C semantics)
+    buckets = f32_exact_buckets(prods)
+    sum_abs = float(prods.abs().to(c.torch.float64).sum().item())
+    del prods, tx, ty
+    c.torch.cuda.empty_cache()
+    parts = d.gather((buckets.tolist(), sum_abs, got))
+    exact = sum((buckets_value(b) for b, _, _ in parts), Fraction(0))
+    check = reduction_check(got, exact, total_n, sum(s for _, s, _ in parts))
+    check["ranks_agree"] = len({g for _, _, g in parts}) == 1
 
-            def step():
-                par.sharded_reduce(kernel, sx, sy, return_device=True, collective=collective,
-                                   overlap_previous=collective == "p2p").free()
-
-        # correctness of the tuned kernel on this data (cheap, before timing)
-        value = kernel(gx, gy)
-        terms_ok = bool(np.isfinite(value))
-        # the tuned kernel against an fp64 oracle on the same data: products
-        # rounded in float32 (C semantics), summed in float64 by numpy
-        terms = np.multiply(hx, hy, dtype=np.float32).astype(np.float64)
-        want = float(np.sum(terms))
-        bound = 0.5 * float(np.spacing(np.float32(abs(want)))) + \
-            2 * n * 2.0**-53 * float(np.abs(terms).sum())
-        check = {"got": float(value), "want_fp64": want, "bound": bound,
-                 "ulps_f32": abs(float(value) - want) / float(np.spacing(np.float32(abs(want)))),
-                 "ok": abs(float(value) - want) <= bound}
-        del terms
-
+    def run_step():
+        step(sx, sy, out=out)
+    if c.collective == "p2p":                # every rank must agree the exchange works
+        run_step()
+        timed_out = 0.0
         try:
-            step()
-            if collective == "p2p":   # every rank must agree the exchange works
-                timed_out = 0.0
-                try:
-                    par.peer_mailbox(None, stream_handle).check(stream_handle)
-                except par.PeerTimeout:
-                    timed_out = 1.0
-                if d.max(timed_out) > 0:
-                    raise RuntimeError("the peer exchange timed out on some rank")
-        except Exception as exc:  # p2p refused or broken here: the NCCL baseline
-            if collective != "p2p":
-                raise
-            print(f"warning: p2p exchange unavailable ({exc}); using NCCL", file=sys.stderr)
-            collective = "auto"
-            step()
-        for _ in range(max(3, args.warmup)):
-            step()
-        rt.synchronize()
-        d.barrier()
-        rt.synchronize()
-        launches0 = kernel.launches
-        with ClockSampler(d.local) as clocks:
-            total_ms, per_step = _time_steps(rt, step, args.steps,
-                                             os.environ.get("RTCG_BENCH_STEP_EVENTS", "0") == "1")
-        # NCCL paths add one combine launch per step; p2p is one kernel
-        launches = kernel.launches - launches0 + (
-            args.steps if d.distributed and collective != "p2p" else 0)
-        rt.synchronize()
-        d.barrier()
-        step_ms = d.max(total_ms / args.steps)
-        kern_ms = float(np.mean(per_step))
-        value_gbs = 8 * total_n / (step_ms * 1e-3) / 1e9
-
-        # e2e through the public API: pinned host -> device, reduce, scalar back
-        e2e_steps = max(2, min(args.steps, 5))
-        h2d = 2 * n * 4
-        gx2, gy2 = pool.alloc_uninitialized(nd.float32, (n,)), pool.alloc_uninitialized(nd.float32, (n,))
-
-        from paper_0911_3456_b200 import driver as drv
-        sx2 = par.ShardedArray(gx2, lo, total_n, d.rank, d.world)
-        sy2 = par.ShardedArray(gy2, lo, total_n, d.rank, d.world)
-
-        def e2e_sequential():
-            gx2.copy_from_host(hx, sync=False)
-            gy2.copy_from_host(hy, sync=False)
-            if d.distributed:           # this rank's slice, then the cross-GPU combine
-                return par.sharded_reduce(kernel, sx2, sy2, collective=collective)
-            return kernel(gx2, gy2)     # returns the host scalar (4-byte DtoH)
-
-        def e2e_streamed():             # dot(driver.In(x), driver.In(y)): chunked, overlapped
-            return kernel(drv.In(hx), drv.In(hy))
-
-        def time_e2e(fn):
-            fn()
-            d.barrier()
-            t0 = time.perf_counter()
-            for _ in range(e2e_steps):
-                fn()
-            return d.max((time.perf_counter() - t0) / e2e_steps)
-        # copy-in then reduce: the inputs cross the link once, whole (the
-        # measured best for a one-way workload; the streamed host call adds
-        # per-chunk overhead and is reported beside it at N = 1)
-        e2e_s = time_e2e(e2e_sequential)
-        streamed_s = None if d.distributed else time_e2e(e2e_streamed)
-        e2e_gbs = 8 * total_n / e2e_s / 1e9
-        # the link roofline for e2e: raw pinned HtoD copy of the same bytes
-        t0 = time.perf_counter()
-        for _ in range(2):
-            gx2.copy_from_host(hx, sync=False)
-            gy2.copy_from_host(hy, sync=True)
-        link_gbs = 2 * h2d / (time.perf_counter() - t0) / 1e9
-        gx2.free()
-        gy2.free()
-
-        workloads = {} if args.quick or d.world > 1 else \
-            secondary_workloads(rt, nd, ew, rd, at, pool, peak)
-
-    algo_bytes = 8 * n
-    achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
-    line = {
-        "metric": METRIC, "value": round(value_gbs, 2), "unit": "GB/s", "n_gpus": d.world,
-        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(step_ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_gpu": n, "n_total": total_n,
-                   "variant": best, "autotune_seconds": round(tune_s, 2),
-                   "autotune_from_store": tuned.from_store,
-                   "l2": "inputs 2 GiB per GPU > 126 MB L2 (no flush needed)",
-                   "parallelism": f"shards{d.world}" + (f"+{collective}" if d.distributed
-                                                        else ""),
-                   "accumulator": "float64",
-                   "launch": "back-to-back steps with programmatic dependent launch (each "
-                             "reduction streams its inputs while the previous one folds)",
-                   "gpu": info["name"], "result_finite": terms_ok,
-                   "result_vs_fp64_oracle": check},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
-                     if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
-                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "nominal_peak": NOMINAL_HBM,
-                     "frac_of_nominal": round(achieved / NOMINAL_HBM, 4),
-                     "traffic": _ncu_traffic("dot_k"),
-                     "kernel": kernel.launch_config(gx, gy)["entry"],
-                     "algorithmic_bytes_per_launch": algo_bytes,
-                     "avg_kernel_ms": round(kern_ms, 4)},
-        "e2e": {"value": round(e2e_gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": 4, "steps": e2e_steps,
-                "path": "GPUArray.copy_from_host (pinned) x2 + "
-                        + ("sharded_reduce" if d.distributed else "ReductionKernel.__call__")
-                        + " (numpy scalar)",
-                "streamed_value": None if streamed_s is None else
-                round(8 * total_n / streamed_s / 1e9, 2),
-                "streamed_path": "ReductionKernel(driver.In(x), driver.In(y)): 64 MiB chunks, "
-                                 "uploads overlapped with per-chunk reductions",
-                "link_h2d_gbs": round(link_gbs, 2),
-                "link_frac": round(e2e_gbs / (link_gbs * d.world), 4),
-                "note": "every input byte crosses the host link once per step, so e2e is "
-                        "bounded by the measured pinned HtoD bandwidth (link_h2d_gbs)"},
-        "gpu_launches": launches,
-        "clocks": clocks.summary(),
-        "workloads": workloads,
-    }
-    if d.world == 1 and d.rank == 0 and not args.no_cpu:
+            par.peer_mailbox(None, 0).check(0)
+        except par.PeerTimeout:
+            timed_out = 1.0
+        if d.max(timed_out) > 0:
+            print("warning: p2p exchange timed out; using NCCL", file=sys.stderr)
+            c.collective = "auto"
+            step, per_step_launches = c.reducer(kernel)
+    mark = {}
+    with ClockSampler(c.bus_id) as clocks:
+        step_ms, per = c.timed(run_step, c.args.steps, warmup=max(3, c.args.warmup),
+                               per_step=os.environ.get("RTCG_BENCH_STEP_EVENTS", "0") == "1",
+                               on_start=lambda: mark.setdefault("launches", kernel.launches))
+    launches = (kernel.launches - mark["launches"]) * per_step_launches
+    # isolated launches (no programmatic overlap, synchronised between): the
+    # kernel's own time, next to the pipelined per-step time
+    iso = []
+    for _ in range(10):
+        s, e = rt.Event(), rt.Event()
+        s.record()
+        kernel.launch(gx, gy, out=out)
+        e.record()
+        e.synchronize()
+        iso.append(s.elapsed_ms(e))
+    if c.collective == "p2p":
         try:
-            base = cpu_reference("dot_k", budget_s=10.0)
-            line["cpu_baseline"] = {k: base[k] for k in ("value", "unit", "cores", "kind",
-                                                         "sample")}
-        except Exception as exc:  # pragma: no cover - report, don't fail the bench
-            line["cpu_baseline"] = {"value": None, "error": str(exc)}
-    if d.rank == 0:
-        emit(line)
-    d.close()
-    return 0
+            par.peer_mailbox(None, 0).check(0)
+            check["peer_timeouts"] = 0
+        except par.PeerTimeout:
+            check["ok"] = False
+            check["peer_timeouts"] = 1
+    res = {"kernel": kernel, "variant": best, "tune": tuned, "step_ms": step_ms,
+           "kern_ms": float(np.mean(per)), "iso_ms": float(np.median(iso)),
+           "launches": launches, "clocks": clocks.summary(), "check": check,
+           "value_gbs": 8 * total_n / (step_ms * 1e-3) / 1e9,
+           "hx": hx, "hy": hy, "gx": gx, "gy": gy, "out": out, "spec": spec, "lo": lo}
+    return res
 
 
-def _ncu_traffic(kernel: str):
-    """dram bytes per launch from the committed ncu summary, if captured."""
-    path = ROOT / "profiles" / "ncu_summary.json"
-    try:
-        data = json.loads(path.read_text())
-        return data["kernels"][kernel]["dram_bytes_per_launch"]
-    except Exception:
-        return None
+def strong_dot(c: Ctx, h: dict) -> dict:
+    """The §7.3 #1 hard case: 2^28 elements in TOTAL, split over the ranks
+    (2^25 per GPU at N=8), same kernel; a slice of the resident inputs."""
+    d, par, nd = c.d, c.par, c.nd
+    total = N_PER_GPU
+    lo, hi = par.shard_range(total, d.rank, d.world)
+    m = hi - lo
+    gx, gy = h["gx"][:m], h["gy"][:m]
+    sx = par.ShardedArray(gx, lo, total, d.rank, d.world)
+    sy = par.ShardedArray(gy, lo, total, d.rank, d.world)
+    kernel = h["kernel"]
+    step, _ = c.reducer(kernel)
+    got = float(c.global_value(kernel, sx, sy))
+    prods = c.torch.as_tensor(gx, device="cuda") * c.torch.as_tensor(gy, device="cuda")
+    parts = d.gather((f32_exact_buckets(prods).tolist(),
+                      float(prods.abs().to(c.torch.float64).sum().item())))
+    del prods
+    c.torch.cuda.empty_cache()
+    exact = sum((buckets_value(b) for b, _ in parts), Fraction(0))
+    check = reduction_check(got, exact, total, sum(s for _, s in parts))
+    ms, _ = c.timed(lambda: step(sx, sy, out=h["out"]), c.args.steps, warmup=3)
+    gbs = 8 * total / (ms * 1e-3) / 1e9
+    return {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / (c.peak * d.world), 4),
+            "n_total": total, "n_per_gpu": m, "parity_ok": check["ok"], "ulps": check["ulps"],
+            "bit_equal_f32_fsum": check["bit_equal_f32_fsum"]}
 
 
-def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
-    """The other BASELINE configs on one GPU: each kernel autotuned over
-    unroll x block (TuneStore-cached), then device-timed (best of 10)."""
+def c4_workloads(c: Ctx) -> dict:
+    """BASELINE configs[3]: max|x| and L2 (f32, x ~ N(0,1)) and the wrapping
+    int64 sum (x ~ U[-2^62, 2^62)) at n = 2^32 in TOTAL, contiguous shards
+    over the ranks, global result through the cross-GPU combine.  Inputs are
+    drawn on the device (torch Philox, seed 1 + rank); each result is checked
+    against an exact reference computed from the same device data."""
+    d, rt, at, ew, nd, par, rd, torch = c.d, c.rt, c.at, c.ew, c.nd, c.par, c.rd, c.torch
+    lo, hi = par.shard_range(N_C4, d.rank, d.world)
+    m = hi - lo
+    out = {}
+    gen = torch.Generator(device="cuda")
+    xf = c.pool.alloc_uninitialized(nd.float32, (m,))
+    tf = torch.as_tensor(xf, device="cuda")
+    gen.manual_seed(1 + d.rank)
+    tf.normal_(generator=gen)
+    sxf = par.ShardedArray(xf, lo, N_C4, d.rank, d.world)
+    o32 = c.pool.alloc_uninitialized(nd.float32, ())
+    axes = dict(at.DEFAULT_AXES, waves=(0, 1, 2))
+    k_steps = max(3, min(c.args.steps, 10))
+
+    def run(name, spec, sx, nbytes, want_fn, note, o):
+        tuned = c.tune_on_rank0(lambda: at.tune_reduction(
+            spec, name, m, axes, args=[sx.local], protocol=c.proto, store=c.store,
+            burst=3).best_assignment)
+        k = rd.ReductionKernel(spec, name, ew.VariantParams(**tuned))
+        step, per = c.reducer(k)
+        got = c.global_value(k, sx)
+        ok, extra = want_fn(got)
+        with ClockSampler(c.bus_id) as clk:
+            ms, _ = c.timed(lambda: step(sx, out=o), k_steps, warmup=2)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out[name] = {"ms": round(ms, 4), "GB/s": round(gbs, 1),
+                     "frac": round(gbs / (c.peak * d.world), 4), "algorithmic_bytes": nbytes,
+                     "n_total": N_C4, "n_per_gpu": m, "parity_ok": ok, "variant": tuned,
+                     "launches_per_step": per, "note": note, "clocks": clk.summary(), **extra}
+
+    # max|x|: exact (max is order independent on NaN-free data)
+    local_max = float(tf.abs().max().item())
+    gmax = max(d.gather(local_max))
+
+    def want_max(got):
+        return float(got) == gmax, {"want": gmax, "got": float(got)}
+    run("maxabs_f32_2p32", rd.ReductionSpec("float *x", nd.float32, "0", "a > b ? a : b",
+                                            "fabsf(x[i])"), sxf, 4 * N_C4, want_max,
+        "max|x|, x ~ N(0,1) float32", o32)
+
+    # L2: sum of float32 squares accumulated in float64; sqrt on the host
+    sq = tf * tf
+    parts = d.gather((f32_exact_buckets(sq).tolist(),
+                      float(sq.to(torch.float64).sum().item())))
+    del sq
+    torch.cuda.empty_cache()
+    exact = sum((buckets_value(b) for b, _ in parts), Fraction(0))
+    sum_abs = sum(s for _, s in parts)
+
+    def want_sumsq(got):
+        chk = reduction_check(float(got), exact, N_C4, sum_abs)
+        return chk["ok"], {"ulps": chk["ulps"], "bit_equal_f32_fsum": chk["bit_equal_f32_fsum"],
+                           "l2": math.sqrt(float(got))}
+    run("sumsq_f32_2p32", rd.ReductionSpec("float *x", nd.float32, "0", "a + b", "x[i] * x[i]"),
+        sxf, 4 * N_C4, want_sumsq, "L2 norm = sqrt(sum of x[i]*x[i]) on the host; x ~ N(0,1)",
+        o32)
+    del tf
+    xf.free()
+
+    xi = c.pool.alloc_uninitialized(nd.int64, (m,))
+    ti = torch.as_tensor(xi, device="cuda")
+    gen.manual_seed(1 + d.rank)
+    ti.random_(-(1 << 62), 1 << 62, generator=gen)
+    sxi = par.ShardedArray(xi, lo, N_C4, d.rank, d.world)
+    want_i = wrap64(sum(d.gather(i64_wrapped_sum(ti))))
+    del ti
+    torch.cuda.empty_cache()
+    o64 = c.pool.alloc_uninitialized(nd.int64, ())
+
+    def want_sum(got):
+        return int(got) == want_i, {"want": want_i, "got": int(got)}
+    run("sum_i64_2p32", rd.ReductionSpec("int64_t *x", nd.int64, "0", "a + b"), sxi, 8 * N_C4,
+        want_sum, "x ~ U[-2^62, 2^62) int64: the sum wraps (bit-exact, order independent)", o64)
+    xi.free()
+    o32.free()
+    o64.free()
+    return out
+
+
+def elementwise_workloads(c: Ctx) -> dict:
+    """axpy f32 and the f64 poly+sin (configs[0] at 2^28, configs[2]), 2^28
+    per GPU on every rank (no communication); timed as max over ranks."""
+    d, rt, at, ew, nd, par = c.d, c.rt, c.at, c.ew, c.nd, c.par
     out = {}
     n = N_PER_GPU
-    rng = np.random.default_rng(1)
-    proto = at.MeasurementProtocol(warmup=1, repeats=3)
-    store = at.TuneStore()
-
-    def best_ms(fn, reps=5, burst=10):
-        """Per-launch time as the headline measures it: the mean of a burst of
-        back-to-back launches between two events (best of ``reps`` bursts)."""
-        fn()
-        rt.synchronize()
-        best = math.inf
-        for _ in range(reps):
-            ms, _ = _time_steps(rt, fn, burst, per_step=False)
-            best = min(best, ms / burst)
-        return best
-
-    def record(name, fn, nbytes, tuned, **extra):
-        with ClockSampler(rt.current_device()) as clk:
-            ms = best_ms(fn)
-        extra = dict(extra, clocks=clk.summary())
-        gbs = nbytes / (ms * 1e-3) / 1e9
-        out[name] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4),
-                     "algorithmic_bytes": nbytes, "variant": tuned.best_assignment,
-                     "tune_from_store": tuned.from_store, **extra}
-
-    x = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
-    y = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
-    z = pool.alloc_uninitialized(nd.float32, (n,))
+    rng = np.random.default_rng([1, d.rank])
+    x = nd.from_host(c.pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
+    y = nd.from_host(c.pool, nd.float32, rng.uniform(-1, 1, n).astype(np.float32))
+    z = c.pool.alloc_uninitialized(nd.float32, (n,))
     sig, op = "float a, float *x, float b, float *y, float *z", "z[i] = a * x[i] + b * y[i]"
     axes = dict(at.DEFAULT_AXES, waves=(0, 1, 2))
-    t = at.tune_elementwise(sig, op, "axpy", n, axes, args=[2.0, x, -3.0, y, z],
-                            protocol=proto, store=store, burst=10)
-    axpy = ew.ElementwiseKernel(sig, op, "axpy", ew.VariantParams(**t.best_assignment))
-    record("axpy_f32_2p28", lambda: axpy(2.0, x, -3.0, y, z), 12 * n, t)
+    best = c.tune_on_rank0(lambda: at.tune_elementwise(
+        sig, op, "axpy", n, axes, args=[2.0, x, -3.0, y, z], protocol=c.proto, store=c.store,
+        burst=10).best_assignment)
+    axpy = ew.ElementwiseKernel(sig, op, "axpy", ew.VariantParams(**best))
+    with ClockSampler(c.bus_id) as clk:
+        ms, _ = c.timed(lambda: axpy(2.0, x, -3.0, y, z), 10)
+    # parity: IEEE float32 with contraction off is what torch computes too
+    tx, ty, tz = (c.torch.as_tensor(a, device="cuda") for a in (x, y, z))
+    ok = bool(c.torch.equal(tz, (tx * 2.0) + (ty * -3.0)))
+    ok = all(d.gather(ok))
+    gbs = 12 * n * d.world / (ms * 1e-3) / 1e9
+    out["axpy_f32_2p28"] = {"ms": round(ms, 4), "GB/s": round(gbs, 1),
+                            "frac": round(gbs / (c.peak * d.world), 4),
+                            "algorithmic_bytes": 12 * n * d.world, "variant": best,
+                            "parity_ok": ok, "clocks": clk.summary()}
+    del tx, ty, tz
     for a in (x, y, z):
         a.free()
 
-    # C4: max|x|, L2 (sum of squares; sqrt on the host) and the wrapping int64
-    # sum at n = 2^32, inputs synthesised on the device from a hash of i
-    big = 1 << 32
-    xf = pool.alloc_uninitialized(nd.float32, (big,))
-    ew.ElementwiseKernel("float *x", "unsigned long h = (unsigned long) i * 0x9E3779B97F4A7C15UL; "
-                         "x[i] = (float) ((long) (h >> 40) - (1L << 23)) * 1.1920929e-7f",
-                         "synth_f32")(xf)
-    o32 = pool.alloc_uninitialized(nd.float32, ())
-    for name, mp, red in (("maxabs", "fabsf(x[i])", "a > b ? a : b"),
-                          ("sumsq", "x[i] * x[i]", "a + b")):
-        spec = rd.ReductionSpec("float *x", nd.float32, "0", red, mp)
-        t = at.tune_reduction(spec, name, big, axes, args=[xf], protocol=proto,
-                              store=store, burst=3)
-        k = rd.ReductionKernel(spec, name, ew.VariantParams(**t.best_assignment))
-        record(f"{name}_f32_2p32", lambda: k.launch(xf, out=o32, overlap_previous=True),
-               4 * big, t,
-               note="L2 norm = sqrt(sumsq) on the host" if name == "sumsq" else "max|x|")
-    xf.free()
-    xi = pool.alloc_uninitialized(nd.int64, (big,))
-    ew.ElementwiseKernel("long *x", "x[i] = (long) ((unsigned long) i * 0x9E3779B97F4A7C15UL) >> 1",
-                         "synth_i64")(xi)
-    o64 = pool.alloc_uninitialized(nd.int64, ())
-    spec = rd.ReductionSpec("int64_t *x", nd.int64, "0", "a + b")
-    t = at.tune_reduction(spec, "sum_k", big, axes, args=[xi], protocol=proto,
-                          store=store, burst=3)
-    si = rd.ReductionKernel(spec, "sum_k", ew.VariantParams(**t.best_assignment))
-    record("sum_i64_2p32", lambda: si.launch(xi, out=o64, overlap_previous=True), 8 * big, t,
-           note="values in [-2^62, 2^62): the sum wraps (bit-exact, order independent)")
-    xi.free()
-
     hx = nd.pinned_empty((n,), nd.float64)
     hx[:] = rng.uniform(-2, 2, n)
-    xd = nd.from_host(pool, nd.float64, hx)
-    zd = pool.alloc_uninitialized(nd.float64, (n,))
+    xd = nd.from_host(c.pool, nd.float64, hx)
+    zd = c.pool.alloc_uninitialized(nd.float64, (n,))
     sig, op = ("double a, double *x, double *z",
                "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
-    # long statements: the software-pipelined loop keeps loads in flight
     ps_axes = dict(axes, waves=(0, 1, 2, 4), prefetch=(False, True))
-    t = at.tune_elementwise(sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
-                            constraints=(lambda a: not a["prefetch"] or a["waves"] > 0,),
-                            protocol=proto, store=store, burst=10)
-    ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**t.best_assignment))
-    record("polysin_f64_2p28", lambda: ps(0.5, xd, zd), 16 * n, t,
-           bound="instruction issue + HBM: ~67 instructions/element (~21 FP64); ncu: issue "
-                 "slots 68% busy, FP64 pipe 44%, DRAM 68.5% (profiles/r01_ncu_full_polysin_*); "
-                 "the prefetch variant keeps the next chunk's loads in flight")
-    # C3 end to end through the public API: pinned host x -> HBM, kernel, HBM ->
-    # pinned host z (16 B/element cross the host link), against the reference's
-    # CPU kernel on all host cores -- the compute-heavy case where the GPU wins
-    # end to end even though every byte crosses PCIe.
-    hz = nd.pinned_empty((n,), nd.float64)
-    from paper_0911_3456_b200 import driver as drv
+    best = c.tune_on_rank0(lambda: at.tune_elementwise(
+        sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
+        constraints=(lambda a: not a["prefetch"] or a["waves"] > 0,),
+        protocol=c.proto, store=c.store, burst=10).best_assignment)
+    ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**best))
+    with ClockSampler(c.bus_id) as clk:
+        ms, _ = c.timed(lambda: ps(0.5, xd, zd), 10)
+    gbs = 16 * n * d.world / (ms * 1e-3) / 1e9
+    # parity at sampled positions against the same expression in float64
+    # with contraction off (torch: sin via libdevice-equivalent; the bound is
+    # the §8c.8 transcendental rule: 2 ulp(sin x) + 1 ulp of the result)
+    idx = c.torch.randint(0, n, (1 << 20,), device="cuda",
+                          generator=c.torch.Generator(device="cuda").manual_seed(5))
+    tx = c.torch.as_tensor(xd, device="cuda")[idx]
+    tz = c.torch.as_tensor(zd, device="cuda")[idx]
+    poly = ((tx * 0.5 + 2.0) * tx - 1.5) * tx
+    s = c.torch.sin(tx)
+    want = poly + s
+    tol = 2 * s.abs() * 2.0 ** -52 + want.abs() * 2.0 ** -52 + 2.0 ** -1074
+    ok = all(d.gather(bool(((tz - want).abs() <= 2 * tol).all().item())))
+    out["polysin_f64_2p28"] = {
+        "ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / (c.peak * d.world), 4),
+        "algorithmic_bytes": 16 * n * d.world, "variant": best, "parity_ok": ok,
+        "parity": "2^20 sampled positions vs float64 torch within 2 ulp(sin)+1 ulp (x2 margin); "
+                  "tests/ pin it to the C oracle",
+        "clocks": clk.summary(),
+        "registers": c.rt.registers(ps.vectorized.function(d.device)) if ps.vectorized else None}
+    # FMA point (north_star allows <= 1 ulp with contraction): same variant
+    try:
+        from paper_0911_3456_b200 import jit
+        cfg = jit.ToolchainConfig(flags=tuple("-fmad=true" if f == "-fmad=false" else f
+                                              for f in jit.DEFAULT_FLAGS))
+        psf = ew.ElementwiseKernel(sig, op, "polysin_fma", ew.VariantParams(**best), config=cfg)
+        msf, _ = c.timed(lambda: psf(0.5, xd, zd), 10)
+        out["polysin_f64_2p28"]["fma"] = {
+            "ms": round(msf, 4), "GB/s": round(16 * n * d.world / (msf * 1e-3) / 1e9, 1),
+            "note": "-fmad=true (contracted); parity mode is the headline"}
+    except Exception as exc:  # noqa: BLE001 - report only
+        out["polysin_f64_2p28"]["fma"] = {"error": str(exc)[:200]}
+    if d.world == 1:
+        out["polysin_f64_2p28"].update(polysin_e2e(c, ps, hx, xd, zd))
+    xd.free()
+    zd.free()
+    return out
 
-    def e2e_sequential():
+
+def polysin_e2e(c: Ctx, ps, hx, xd, zd) -> dict:
+    """C3 end to end through the public API: pinned host x -> HBM, kernel,
+    HBM -> pinned host z (16 B/element cross the host link), against the
+    reference's CPU kernel on all host cores on a bounded sample."""
+    nd = c.nd
+    from paper_0911_3456_b200 import driver as drv
+    n = hx.size
+    hz = nd.pinned_empty((n,), nd.float64)
+
+    def sequential():
         xd.copy_from_host(hx, sync=False)
         ps(0.5, xd, zd)
         zd.to_host(out=hz)
 
-    def e2e_streamed():           # chunked upload / kernel / download on two streams
+    def streamed():           # chunked upload / kernel / download on two streams
         ps(0.5, drv.In(hx), drv.Out(hz))
 
     def timed(fn, reps=3):
@@ -598,19 +876,19 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
         for _ in range(reps):
             fn()
         return (time.perf_counter() - t0) / reps
-    seq_s, str_s = timed(e2e_sequential), timed(e2e_streamed)
-    out["polysin_f64_2p28"]["e2e"] = {
+    seq_s, str_s = timed(sequential), timed(streamed)
+    res = {"e2e": {
         "value": round(16 * n / str_s / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
         "d2h_bytes_per_step": 8 * n, "steps": 3,
         "path": "ElementwiseKernel(0.5, driver.In(x), driver.Out(z)) on pinned host arrays: "
                 "64 MiB chunks, upload / kernel / download overlapped on two streams",
         "sequential_value": round(16 * n / seq_s / 1e9, 2),
-        "sequential_path": "GPUArray.copy_from_host + ElementwiseKernel + GPUArray.to_host"}
+        "sequential_path": "GPUArray.copy_from_host + ElementwiseKernel + GPUArray.to_host"}}
     try:
         from oracle import refdrive
         fn, kind = refdrive.load("polysin")
-        threads = refdrive.host_threads()
-        m = 1 << 23
+        threads = host_threads()
+        m = 1 << 24
         cx, cz = np.ascontiguousarray(hx[:m]), np.empty(m)
         fn(0.5, cx, cz, workers=threads)
         best = math.inf
@@ -618,24 +896,347 @@ def secondary_workloads(rt, nd, ew, rd, at, pool, peak):
             t0 = time.perf_counter()
             fn(0.5, cx, cz, workers=threads)
             best = min(best, time.perf_counter() - t0)
-        out["polysin_f64_2p28"]["cpu_baseline"] = {
+        res["cpu_baseline"] = {
             "value": round(16 * m / best / 1e9, 3), "unit": "GB/s", "cores": threads,
-            "kind": kind, "sample": f"polysin f64 n=2^23 (bounded sample), x~U(-2,2), "
-                                    f"reference variant, {threads} worker threads, best of 5"}
+            "kind": kind, "sample": f"polysin f64 n=2^24 (bounded sample: the first 2^24 of "
+                                    f"the same x), reference variant, {threads} worker "
+                                    f"threads, best of 5 after 1 warm-up"}
     except Exception as exc:  # pragma: no cover - report, don't fail the bench
-        out["polysin_f64_2p28"]["cpu_baseline"] = {"value": None, "error": str(exc)}
-    xd.free()
-    zd.free()
-    return out
+        res["cpu_baseline"] = {"value": None, "error": str(exc)}
+    return res
+
+
+def c5_sweep(c: Ctx) -> dict:
+    """BASELINE configs[4], bounded: n in {2^16, 2^20, 2^24, 2^28, 2^32}
+    (total, sharded over the ranks) x dtypes {i32, i64, f32, f64} x ops
+    {x+y, eager chain (x*2 + y) - x, fused chain, sum, max, dot}; device
+    time per call (best of 5 after a warm-up, max over ranks); sizes whose
+    three arrays fit in L2 are flagged.  Plus compile latency (cold NVRTC vs
+    warm cache construction) and an autotune campaign vs its store hit."""
+    d, rt, at, ew, nd, par, rd = c.d, c.rt, c.at, c.ew, c.nd, c.par, c.rd
+    from paper_0911_3456_b200 import fusion, jit
+    res = {"latency": {}, "autotune": {}, "rows": {}}
+    if d.rank == 0:
+        cold_root = Path(tempfile.mkdtemp(prefix="rtcg-cold-"))
+        cold, warm = [], []
+        sources = [("double *x, double *z", f"z[i] = {k} * x[i] + {k + 1}") for k in range(8)]
+        for k, (sig, op) in enumerate(sources):        # scripts/cache_latency.py recipe
+            t0 = time.perf_counter()
+            ew.ElementwiseKernel(sig, op, f"affine_{k}", cache=jit.CacheStore(cold_root))
+            cold.append(time.perf_counter() - t0)
+        for k, (sig, op) in enumerate(sources):
+            t0 = time.perf_counter()
+            ew.ElementwiseKernel(sig, op, f"affine_{k}", cache=jit.CacheStore(cold_root))
+            warm.append(time.perf_counter() - t0)
+        res["latency"] = {"cold_nvrtc_construct_ms_median": round(np.median(cold) * 1e3, 2),
+                          "warm_cache_construct_ms_median": round(np.median(warm) * 1e3, 3),
+                          "cold_over_warm": round(float(np.median(cold) / np.median(warm)), 1),
+                          "kernels": len(sources)}
+        store = at.TuneStore(tempfile.mkdtemp(prefix="rtcg-tune-"))
+        spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
+        t0 = time.perf_counter()
+        r = at.tune_reduction(spec, "dot_c5", 1 << 26, at.DEFAULT_AXES, store=store, pool=c.pool)
+        campaign = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r2 = at.tune_reduction(spec, "dot_c5", 1 << 26, at.DEFAULT_AXES, store=store,
+                               pool=c.pool)
+        res["autotune"] = {"problem": "dot f32 n=2^26", "variants": len(r.table),
+                           "campaign_s": round(campaign, 2),
+                           "store_hit_s": round(time.perf_counter() - t0, 4),
+                           "store_hit_same_best": r2.best_assignment == r.best_assignment}
+    d.barrier()
+
+    def dev_ms(fn, reps=5):
+        fn()
+        rt.synchronize()
+        d.barrier()
+        s, e = rt.Event(), rt.Event()
+        best = math.inf
+        for _ in range(reps):
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_ms(e))
+        d.barrier()
+        return d.max(best)
+
+    chain = fusion.fused(lambda p, q: (p * 2 + q) - p)
+    l2 = c.info.get("l2_bytes") or (126 << 20)
+    # HBM budget per rank: ranks sharing a GPU split it
+    per_gpu = max(1, d.world // max(1, rt.device_count())) if d.shared_gpu else 1
+    budget = min(100 << 30, int(0.8 * c.info["total_mem"]) // per_gpu)
+    c.torch.cuda.empty_cache()
+    ok_all = True
+    for dname in ("int32", "int64", "float32", "float64"):
+        dt = nd.BY_NAME[dname]
+        cn = dt.cname
+        fill = ew.ElementwiseKernel(
+            f"long seed, {cn} *x",
+            f"x[i] = ({cn}) ((long) (((unsigned long) i * 2654435761UL + seed) % 2001) - 1000)"
+            f" / ({cn}) {'1000.0' if dt.kind == 'f' else '1'}", f"fill_{dname}")
+        add = ew.ElementwiseKernel(f"{cn} *x, {cn} *y, {cn} *z", "z[i] = x[i] + y[i]",
+                                   f"add_{dname}")
+        kernels = {"sum": rd.sum_kernel(dt), "max": rd.max_kernel(dt), "dot": rd.dot_kernel(dt)}
+        for lg in (16, 20, 24, 28, 32):
+            total = 1 << lg
+            lo, hi = par.shard_range(total, d.rank, d.world)
+            m = hi - lo
+            key = f"{dname}_2p{lg}"
+            if 3 * dt.size * m > budget:                 # x, y, z
+                res["rows"][key] = {"skipped": f"needs > {budget >> 30} GiB per rank"}
+                continue
+            x = c.pool.alloc_uninitialized(dt, (m,))
+            y = c.pool.alloc_uninitialized(dt, (m,))
+            z = c.pool.alloc_uninitialized(dt, (m,))
+            fill(1, x, base=lo)
+            fill(7, y, base=lo)
+            sx, sy = (par.ShardedArray(a, lo, total, d.rank, d.world) for a in (x, y))
+            row = {"l2_resident": 3 * dt.size * m <= l2}
+            gb = lambda nbytes, ms: round(nbytes * d.world / ms / 1e6, 1)  # noqa: E731
+            ms = dev_ms(lambda: add(x, y, z))
+            row["add_us"], row["add_GBs"] = round(ms * 1e3, 2), gb(3 * dt.size * m, ms)
+            if 5 * dt.size * m <= budget:               # + two eager temporaries
+
+                def eager():
+                    t1 = x * 2
+                    t2 = t1 + y
+                    t3 = t2 - x
+                    for t in (t1, t2, t3):
+                        t.free()
+                ms = dev_ms(eager)
+                row["chain_eager_us"], row["chain_eager_GBs"] = round(ms * 1e3, 2), \
+                    gb(3 * dt.size * m, ms)
+
+            def fused_chain():
+                chain(x, y).free()
+            ms = dev_ms(fused_chain)
+            row["chain_fused_us"], row["chain_fused_GBs"] = round(ms * 1e3, 2), \
+                gb(3 * dt.size * m, ms)
+            for name, k in kernels.items():
+                args = (sx, sy) if name == "dot" else (sx,)
+                step, _ = c.reducer(k)
+                o = c.pool.alloc_uninitialized(k.spec.out_dtype, ())
+                ms = dev_ms(lambda: step(*args, out=o))
+                nb = (2 if name == "dot" else 1) * dt.size * m
+                row[f"{name}_us"], row[f"{name}_GBs"] = round(ms * 1e3, 2), gb(nb, ms)
+                o.free()
+            # integer rows: exact checks of the global results vs torch
+            if dt.kind == "i":
+                t = c.torch.as_tensor(x, device="cuda")
+                want_s = wrap64(sum(d.gather(i64_wrapped_sum(t))))
+                want_m = max(d.gather(int(t.max().item())))
+                got_s = int(c.global_value(kernels["sum"], sx))
+                got_m = int(c.global_value(kernels["max"], sx))
+                bits = dt.size * 8
+                want_s = ((want_s + (1 << (bits - 1))) % (1 << bits)) - (1 << (bits - 1))
+                row["parity_ok"] = got_s == want_s and got_m == want_m
+                ok_all &= row["parity_ok"]
+                del t
+                c.torch.cuda.empty_cache()
+            for a in (x, y, z):
+                a.free()
+            res["rows"][key] = row
+    res["parity_ok"] = ok_all
+    return res
+
+
+def headline_e2e(c: Ctx, h: dict) -> dict:
+    """e2e through the public API: every step uploads this rank's pinned host
+    slices, reduces (with the cross-GPU combine at N > 1) and reads the
+    scalar back; wall time, max over ranks."""
+    d, nd, par = c.d, c.nd, c.par
+    from paper_0911_3456_b200 import driver as drv
+    n = N_PER_GPU
+    total_n = n * d.world
+    kernel = h["kernel"]
+    hx, hy = h["hx"], h["hy"]
+    gx2, gy2 = c.pool.alloc_uninitialized(nd.float32, (n,)), \
+        c.pool.alloc_uninitialized(nd.float32, (n,))
+    sx2 = par.ShardedArray(gx2, h["lo"], total_n, d.rank, d.world)
+    sy2 = par.ShardedArray(gy2, h["lo"], total_n, d.rank, d.world)
+    e2e_steps = max(2, min(c.args.steps, 5))
+
+    def sequential():
+        gx2.copy_from_host(hx, sync=False)
+        gy2.copy_from_host(hy, sync=False)
+        if d.distributed:           # this rank's slice, then the cross-GPU combine
+            return par.sharded_reduce(kernel, sx2, sy2, collective=c.collective)
+        return kernel(gx2, gy2)     # returns the host scalar (4-byte DtoH)
+
+    def streamed():                 # dot(driver.In(x), driver.In(y)): chunked, overlapped
+        return kernel(drv.In(hx), drv.In(hy))
+
+    def time_e2e(fn):
+        fn()
+        d.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            fn()
+        return d.max((time.perf_counter() - t0) / e2e_steps)
+    e2e_s = time_e2e(sequential)
+    streamed_s = None if d.distributed else time_e2e(streamed)
+    d.barrier()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        gx2.copy_from_host(hx, sync=False)
+        gy2.copy_from_host(hy, sync=True)
+    link = d.gather(2 * 8 * n / (time.perf_counter() - t0) / 1e9)
+    gx2.free()
+    gy2.free()
+    e2e_gbs = 8 * total_n / e2e_s / 1e9
+    return {"value": round(e2e_gbs, 2), "unit": "GB/s", "h2d_bytes_per_step": 8 * n * d.world,
+            "d2h_bytes_per_step": 4 * d.world, "steps": e2e_steps,
+            "path": "GPUArray.copy_from_host (pinned, this rank's slice) x2 + "
+                    + ("parallel.sharded_reduce" if d.distributed else "ReductionKernel.__call__")
+                    + " (numpy scalar)",
+            "streamed_value": None if streamed_s is None else
+            round(8 * total_n / streamed_s / 1e9, 2),
+            "streamed_path": "ReductionKernel(driver.In(x), driver.In(y)): 64 MiB chunks, "
+                             "uploads overlapped with per-chunk reductions",
+            "link_h2d_gbs": round(float(np.mean(link)), 2),
+            "link_h2d_gbs_x_ranks": round(float(np.sum(link)), 2),
+            "link_frac": round(e2e_gbs / float(np.sum(link)), 4),
+            "note": "every input byte crosses a host link once per step; each rank uses its own "
+                    "GPU's link, so e2e is bounded by the sum of the ranks' pinned HtoD "
+                    "bandwidths (link_h2d_gbs_x_ranks)"}
+
+
+def _ncu_traffic(kernel: str, variant: dict):
+    """dram bytes per launch from the committed ncu summary, with the variant
+    it was captured on (and whether that is the variant timed here)."""
+    path = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        data = json.loads(path.read_text())
+        k = data["kernels"][kernel]
+        captured = k.get("bench_variant") or {}
+        same = all(captured.get(a) == variant.get(a) for a in ("block", "unroll", "waves",
+                                                               "cache")) if captured else False
+        return k["dram_bytes_per_launch"], captured, same, data.get("round")
+    except Exception:
+        return None, None, False, None
+
+
+def run_ours(args) -> int:
+    from paper_0911_3456_b200 import _runtime as rt
+    d = Dist(args.gpus, rt.device_count())
+    c = Ctx(args, d)
+    stream = 0          # the legacy default stream: torch's current stream here too
+    with rt.use_stream(stream):
+        c.collective = choose_collective(c)
+        h = headline_dot(c)
+        workloads = {}
+        if not args.quick:
+            workloads["dot_strong_2p28_total"] = strong_dot(c, h)
+        e2e = headline_e2e(c, h)
+        cpu = None
+        if d.world == 1 and d.rank == 0 and not args.no_cpu:
+            try:
+                cpu = cpu_reference(h["hx"], h["hy"])
+            except Exception as exc:  # pragma: no cover - report, don't fail the bench
+                cpu = {"value": None, "error": str(exc)}
+        for a in (h["gx"], h["gy"]):
+            a.free()
+        if not args.quick:
+            workloads.update(c4_workloads(c))
+            workloads.update(elementwise_workloads(c))
+            if not args.no_c5:
+                workloads["c5"] = c5_sweep(c)
+
+    check = h["check"]
+    algo_bytes = 8 * N_PER_GPU
+    achieved = algo_bytes / (h["kern_ms"] * 1e-3) / 1e9
+    traffic, traffic_variant, traffic_same, traffic_round = _ncu_traffic("dot_k", h["variant"])
+    v = h["variant"]
+    parity = {"dot_ok": check["ok"], "dot_ulps": check["ulps"],
+              "dot_bit_equal_f32_fsum": check["bit_equal_f32_fsum"],
+              "dot_ranks_agree": check["ranks_agree"]}
+    for name, w in workloads.items():
+        if isinstance(w, dict) and "parity_ok" in w:
+            parity[f"{name}_ok"] = w["parity_ok"]
+            if "ulps" in w:
+                parity[f"{name}_ulps"] = w["ulps"]
+    parity_ok = all(val for key, val in parity.items() if key.endswith("_ok"))
+    config = workload_config(d.world)
+    config.update({
+        "variant_block": v.get("block"), "variant_unroll": v.get("unroll"),
+        "variant_waves": v.get("waves"), "variant_cache": v.get("cache", "default"),
+        "autotune_seconds": h["tune"]["seconds"], "autotune_from_store": h["tune"]["from_store"],
+        "l2": "inputs 2 GiB per GPU > 126 MB L2 (no flush needed)",
+        "parallelism": f"shards{d.world}" + (f"+{c.collective}" if d.distributed else ""),
+        "backend": d.backend or "none", "shared_gpu": d.shared_gpu,
+        "accumulator": "float64",
+        "launch": "back-to-back steps with programmatic dependent launch (each reduction "
+                  "streams its inputs while the previous one folds)",
+        "gpu": c.info["name"], "parity_ok": parity_ok,
+        "dot_result": check["want"] if check["ok"] else None,
+        "dot_ulps_f32": check["ulps"], "dot_bit_equal_f32_fsum": check["bit_equal_f32_fsum"]})
+    for name in ("maxabs_f32_2p32", "sumsq_f32_2p32", "sum_i64_2p32"):
+        if name in workloads:
+            config[f"c4_{name}_gbs"] = workloads[name]["GB/s"]
+    if "dot_strong_2p28_total" in workloads:
+        config["strong_dot_gbs"] = workloads["dot_strong_2p28_total"]["GB/s"]
+    line = {
+        "metric": METRIC, "value": round(h["value_gbs"], 2), "unit": "GB/s", "n_gpus": d.world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(h["step_ms"], 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "n_ranks_seen": len(d.gather(d.rank)),
+        "collective": c.collective or "none", "parity_ok": parity_ok,
+        "config": config,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": c.peak,
+                     "peak_kind": f"{c.peak_kind} (MEASURED_PEAKS.json hbm_gbs, copy)"
+                     if c.peak_kind == "measured" else "fallback (B200_PROFILING.md)",
+                     "unit": "GB/s", "frac": round(achieved / c.peak, 4),
+                     "ncu_dram_peak": NCU_DRAM_PEAK,
+                     "frac_of_ncu_dram_peak": round(achieved / NCU_DRAM_PEAK, 4),
+                     "traffic": traffic, "traffic_variant": traffic_variant,
+                     "traffic_is_timed_variant": traffic_same, "traffic_round": traffic_round,
+                     "kernel": "dot_k",
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "avg_kernel_ms": round(h["kern_ms"], 4),
+                     "isolated_launch_ms": round(h["iso_ms"], 4),
+                     "isolated_frac": round(algo_bytes / (h["iso_ms"] * 1e-3) / 1e9 / c.peak, 4),
+                     "note": "avg_kernel_ms = per-step time of back-to-back overlapped launches "
+                             "(the timed steps); isolated_launch_ms = median of 10 single "
+                             "launches with a synchronisation between"},
+        "e2e": e2e,
+        "gpu_launches": h["launches"],
+        "clocks": h["clocks"],
+        "parity": parity,
+        "workloads": workloads,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = {k: cpu.get(k) for k in ("value", "unit", "cores", "kind",
+                                                        "sample")}
+        if "error" in cpu:
+            line["cpu_baseline"]["error"] = cpu["error"]
+    if d.rank == 0:
+        emit(line)
+    d.close()
+    return 0 if parity_ok else 3
 
 
 _JSON_OUT = None
 
 
+def _jsonable(obj):
+    if isinstance(obj, dict):
+        return {k: _jsonable(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [_jsonable(v) for v in obj]
+    if isinstance(obj, (np.bool_,)):
+        return bool(obj)
+    if isinstance(obj, np.integer):
+        return int(obj)
+    if isinstance(obj, np.floating):
+        return float(obj)
+    return obj
+
+
 def emit(line: dict) -> None:
     """Write the one JSON result line to the real stdout (native libraries --
     NCCL's version banner, for one -- were redirected to stderr)."""
-    text = json.dumps(line) + "\n"
+    text = json.dumps(_jsonable(line)) + "\n"
     if _JSON_OUT is None:
         sys.stdout.write(text)
         sys.stdout.flush()
@@ -650,18 +1251,27 @@ def _isolate_stdout() -> None:
     os.dup2(2, 1)
 
 
-def main(argv=None) -> int:
+def parse_args(argv=None):
     p = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=200)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--quick", action="store_true", help="skip the secondary workloads")
+    p.add_argument("--quick", action="store_true", help="headline only (no other workloads)")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
-    args = p.parse_args(argv)
-    _isolate_stdout()
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 sweep")
+    return p.parse_args(argv)
+
+
+def main(argv=None) -> int:
+    argv = list(sys.argv[1:] if argv is None else argv)
+    args = parse_args(argv)
     if args.impl == "reference":
+        _isolate_stdout()
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(argv, args.gpus)
+    _isolate_stdout()
     return run_ours(args)
 
 

@@ -42,3 +42,86 @@ def test_gpu_arm_line():
     assert line["gpu_launches"] == 20
     assert line["e2e"]["h2d_bytes_per_step"] == 2 * 4 * (1 << 28)
     assert set(line["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert line["parity_ok"] is True and line["parity"]["dot_ok"] is True
+    assert line["roofline"]["isolated_launch_ms"] > 0
+    assert line["config"]["variant_block"] in (128, 256, 512, 1024)
+
+
+@pytest.mark.gpu
+def test_gpu_arm_spawns_two_ranks_on_one_gpu():
+    """``--gpus 2`` with no launcher: two ranks (sharing the one B200 over
+    gloo), one line, n_gpus 2, parity checked across the ranks."""
+    line = _run("--gpus", "2", "--steps", "5", "--warmup", "3", "--quick", "--no-cpu")
+    assert line["n_gpus"] == 2 and line["n_ranks_seen"] == 2
+    assert line["config"]["n_total"] == 2 << 28 and line["config"]["shared_gpu"] is True
+    assert line["parity_ok"] is True and line["parity"]["dot_ranks_agree"] is True
+    assert line["collective"] in ("auto", "allgather", "allreduce")
+
+
+def test_spawn_env_sets_the_launcher_variables():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    env = bench.spawn_env({"PATH": "/bin"}, 3, 8, 12345)
+    assert env["RANK"] == env["LOCAL_RANK"] == "3" and env["WORLD_SIZE"] == "8"
+    assert env["LOCAL_WORLD_SIZE"] == "8" and env["MASTER_ADDR"] == "127.0.0.1"
+    assert env["MASTER_PORT"] == "12345" and env["PATH"] == "/bin"
+
+
+def test_spawn_ranks_runs_world_processes_and_relays_rank0(tmp_path, capsys):
+    """``bench.py --gpus N`` without a launcher must start N ranks
+    (not silently one).  A stand-in rank script reports what it was given."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    script = tmp_path / "rank.py"
+    script.write_text(
+        "import json, os, sys, torch.distributed as dist\n"
+        "dist.init_process_group('gloo')\n"
+        "ranks = [None] * dist.get_world_size()\n"
+        "dist.all_gather_object(ranks, int(os.environ['RANK']))\n"
+        "if dist.get_rank() == 0:\n"
+        "    print(json.dumps({'n_ranks_seen': len(ranks), 'ranks': ranks,\n"
+        "                      'argv': sys.argv[1:]}))\n"
+        "dist.destroy_process_group()\n")
+    rc = bench.spawn_ranks(["--gpus", "3"], 3, timeout=120, script=str(script))
+    assert rc == 0
+    line = json.loads(capsys.readouterr().out.strip())
+    assert line == {"n_ranks_seen": 3, "ranks": [0, 1, 2], "argv": ["--gpus", "3"]}
+
+
+def test_spawn_ranks_reports_a_failing_rank(tmp_path, capsys):
+    sys.path.insert(0, str(ROOT))
+    import bench
+    script = tmp_path / "fail.py"
+    script.write_text("import os, sys\nsys.exit(7 if os.environ['RANK'] == '1' else 0)\n")
+    assert bench.spawn_ranks([], 2, timeout=60, script=str(script)) == 7
+
+
+def test_exact_checkers_match_fsum_and_python_ints():
+    import math
+    import numpy as np
+    import torch
+    sys.path.insert(0, str(ROOT))
+    import bench
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, 200_003).astype(np.float32)
+    y = rng.uniform(-1, 1, 200_003).astype(np.float32)
+    p = x * y
+    p[:5] = [0.0, 1e-45, -3e-39, 3.0e38, -3.0e38]         # zero, subnormals, huge
+    exact = bench.buckets_value(bench.f32_exact_buckets(torch.from_numpy(p)))
+    assert float(exact) == math.fsum(p.astype(np.float64).tolist())
+    chk = bench.reduction_check(float(np.float32(float(exact))), exact, p.size,
+                                float(np.abs(p.astype(np.float64)).sum()))
+    assert chk["ok"] and chk["bit_equal_f32_fsum"] and chk["ulps"] <= 0.5
+    v = rng.integers(-(1 << 62), 1 << 62, size=100_001, dtype=np.int64)
+    want = sum(int(a) for a in v)
+    assert bench.i64_wrapped_sum(torch.from_numpy(v)) == want
+    assert bench.wrap64(want) == int(v.sum())                # numpy wraps too
+    small = torch.from_numpy(rng.integers(-5, 5, size=1000, dtype=np.int32))
+    assert bench.i64_wrapped_sum(small) == int(small.sum())
+
+
+def test_workload_config_is_shared_by_both_arms():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    assert bench.workload_config(1)["n_total"] == 1 << 28
+    assert bench.workload_config(8)["n_total"] == 8 << 28
