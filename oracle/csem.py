@@ -110,3 +110,40 @@ def float_reduction_bound(terms, result_dtype: str) -> float:
 
 def exact_sum(terms) -> float:
     return math.fsum(np.asarray(terms, dtype=np.float64).tolist())
+
+
+# --- exact sums of float32 values at any n (what math.fsum gives, in seconds) ---------------
+#
+# A float32 value is m * 2^(e-24) with an integer |m| < 2^24 (frexp).  Summing
+# the integer mantissas per exponent is exact in float64 while a bucket's sum
+# stays below 2^53 (chunks of <= 2^28 values); buckets are carried in int64
+# across chunks and combined in Python integers.
+
+_EOFF, _EBINS = 160, 320
+
+
+def f32_buckets(values, chunk: int = 1 << 24) -> np.ndarray:
+    """Per-exponent integer mantissa sums of float32 values (exact)."""
+    values = np.asarray(values, dtype=np.float32).reshape(-1)
+    total = np.zeros(_EBINS, np.int64)
+    for lo in range(0, values.size, chunk):
+        m, e = np.frexp(values[lo:lo + chunk])
+        mi = np.ldexp(m.astype(np.float64), 24)
+        total += np.bincount(e.astype(np.int64) + _EOFF, weights=mi,
+                             minlength=_EBINS).astype(np.int64)
+    return total
+
+
+def buckets_fraction(buckets):
+    from fractions import Fraction
+    num = 0
+    for k, s in enumerate(np.asarray(buckets, dtype=np.int64).tolist()):
+        if s:
+            num += int(s) << k
+    return Fraction(num, 1 << (_EOFF + 24))
+
+
+def exact_f32_sum(values) -> float:
+    """Correctly rounded float64 of the exact sum of float32 values --
+    ``math.fsum(values)`` without a Python loop."""
+    return float(buckets_fraction(f32_buckets(values)))

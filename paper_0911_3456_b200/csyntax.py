@@ -24,7 +24,7 @@ __all__ = [
     "substitute", "render", "CType", "CNode", "Raw", "Lit", "Ident", "Index",
     "BinOp", "Call", "Assign", "Decl", "Block", "For", "If", "Param",
     "FunctionDef", "TranslationUnit", "counted_for", "emit",
-    "unrolled_add_template", "unrolled_add_ast",
+    "unrolled_add_template", "unrolled_add_ast", "UNROLLED_ADD_TEMPLATE",
 ]
 
 
@@ -492,6 +492,10 @@ extern "C" __global__ void ${name}(const ${ctype} *x, const ${ctype} *y, ${ctype
     }
 {% endif %}}
 """
+
+
+# the reference's name for the Fig. 4a template (src/csyntax.py:535)
+UNROLLED_ADD_TEMPLATE = UNROLLED_ADD_CUDA
 
 
 def unrolled_add_template(unroll: int, ctype: str = "float", name: str = "vadd_unrolled") -> str:

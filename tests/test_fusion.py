@@ -118,3 +118,103 @@ def test_fused_reduction_is_one_pass_without_temporaries(pool):
     assert float(r) == 4.5 * n and isinstance(r, np.float64)   # Python float scalar -> f64
     with pytest.raises(ValueError):
         fusion.reduce(fusion.lazy(x), "prod")
+
+
+# --- fused chains against the C oracle (not against the eager GPU chain) --------
+
+from oracle import chain as och, cport  # noqa: E402
+
+PAIRS = [("float32", "float32"), ("int8", "float32"), ("int16", "uint8"), ("int32", "float64"),
+         ("uint32", "int64"), ("float32", "float64"), ("int8", "int8"), ("uint64", "int32"),
+         ("int64", "int64"), ("uint16", "uint16")]
+CHAINS = [lambda p, q: (p * 2 + q) - p,
+          lambda p, q: (p + q) * (q - p) / 3,
+          lambda p, q: 7 - p * q + 0.25,
+          lambda p, q: p * np.float32(1.5) - q / 2,
+          lambda p, q: (q - 100) / (p + 1) * p,
+          lambda p, q: 2.5 / (q * q + 1) + np.int16(3) * p]
+
+
+def _operands(a_name, b_name, n, seed=11):
+    rng = np.random.default_rng(seed)
+    out = []
+    for name in (a_name, b_name):
+        d = np.dtype(name)
+        v = rng.uniform(-3, 3, n) if d.kind == "f" else rng.integers(1, 100, n)
+        out.append(v.astype(d))
+    return out
+
+
+def _fused_source(expr):
+    """Signature and statement of the kernel ``fusion`` generates for expr."""
+    key, arrays, scalars = expr._leaves()
+    params = [f"{a.dtype.cname} *rtcg_fa{k}" for k, a in enumerate(arrays)]
+    params += [f"{sd.cname} rtcg_fs{k}" for k, (_, sd) in enumerate(scalars)]
+    params.append(f"{expr.dtype.cname} *rtcg_fo")
+    return ", ".join(params), "rtcg_fo[i] = " + fusion._render(key, "[i]") + ";", arrays, scalars
+
+
+@pytest.mark.parametrize("a_name, b_name", PAIRS)
+def test_fused_text_has_eager_c_semantics(a_name, b_name):
+    """Host-only: the statement the fuser renders, compiled as C by the
+    oracle, stores exactly what the reference's eager operator chain stores
+    (each operator a separate reference kernel, src/elementwise.py:528-576)."""
+    n = 4099
+    ha, hb = _operands(a_name, b_name, n)
+    pool = host_pool()
+    x, y = pool.alloc(nd.BY_NAME[a_name], (n,)), pool.alloc(nd.BY_NAME[b_name], (n,))
+    for chain in CHAINS:
+        try:
+            want = chain(och.HostArray(ha), och.HostArray(hb)).values
+        except ZeroDivisionError:
+            continue
+        expr = chain(fusion.lazy(x), fusion.lazy(y))
+        assert expr.dtype.name == want.dtype.name
+        sig, stmt, arrays, scalars = _fused_source(expr)
+        host = {id(x): ha, id(y): hb}
+        got = np.zeros(n, want.dtype)
+        cport.Elementwise(sig, stmt, "fused")(*[host[id(a)] for a in arrays],
+                                              *[v for v, _ in scalars], got)
+        assert got.tobytes() == want.tobytes(), (a_name, b_name, stmt)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("a_name, b_name", PAIRS)
+def test_fused_and_eager_gpu_chains_equal_the_oracle(pool, a_name, b_name):
+    n = 100_003
+    ha, hb = _operands(a_name, b_name, n)
+    x, y = nd.from_host(pool, nd.BY_NAME[a_name], ha), nd.from_host(pool, nd.BY_NAME[b_name], hb)
+    for chain in CHAINS:
+        try:
+            want = chain(och.HostArray(ha), och.HostArray(hb)).values
+        except ZeroDivisionError:
+            continue
+        fused = fusion.fused(chain)(x, y).get()
+        eager = chain(x, y).get()
+        assert fused.tobytes() == want.tobytes() == eager.tobytes(), (a_name, b_name)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dname", ["int8", "int32", "int64", "uint16", "float32", "float64"])
+def test_fused_reductions_equal_the_oracle(pool, dname):
+    """reduce(chain) against the reference's stock reductions folded
+    sequentially over the oracle's eager chain: integers and max/min bit for
+    bit; float sums within the fp64-accumulation bound."""
+    from oracle import csem
+    d = nd.BY_NAME[dname]
+    rng = np.random.default_rng(12)
+    n = 1_000_003
+    hx = rng.integers(-50, 50, n).astype(d.np) if d.kind != "f" else \
+        rng.uniform(-1, 1, n).astype(d.np)
+    hy = rng.integers(0, 7, n).astype(d.np) if d.kind != "f" else \
+        rng.uniform(-1, 1, n).astype(d.np)
+    x, y = nd.from_host(pool, d, hx), nd.from_host(pool, d, hy)
+    terms = ((och.HostArray(hx) * 3 + och.HostArray(hy)) - och.HostArray(hx)).values
+    for op in ("sum", "max", "min"):
+        got = fusion.reduce((fusion.lazy(x) * 3 + y) - x, op).get()
+        want = och.reduce(terms, op)
+        assert got.dtype == want.dtype
+        if op == "sum" and d.kind == "f":
+            assert abs(float(got) - float(want)) <= 2 * csem.float_reduction_bound(terms, dname)
+        else:
+            assert got.tobytes() == np.asarray(want).tobytes(), (op, got, want)
