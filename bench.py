@@ -769,6 +769,24 @@ def c4_workloads(c: Ctx) -> dict:
     return out
 
 
+def confirm_best(c: Ctx, tuned, build, run, top: int = 8, burst: int = 30) -> dict:
+    """The tuner's ``top`` variants re-timed over longer bursts of
+    back-to-back launches (how the timed steps run): its 3 x 10-launch
+    samples, taken after earlier workloads heated the GPU, leave a few %
+    of noise in the ranking.  Returns the winning assignment."""
+    finalists = sorted((e for e in tuned.table if e.status == "ok"),
+                       key=lambda e: e.stat_seconds)[:top]
+    best, best_ms = tuned.best_assignment, math.inf
+    for e in finalists:
+        k = build(e.as_dict())
+        timer = c.at.device_timer(lambda k=k: run(k), burst)
+        timer()
+        ms = min(timer() for _ in range(2))
+        if ms < best_ms:
+            best, best_ms = e.as_dict(), ms
+    return best
+
+
 def elementwise_workloads(c: Ctx) -> dict:
     """axpy f32 and the f64 poly+sin (configs[0] at 2^28, configs[2]), 2^28
     per GPU on every rank (no communication); timed as max over ranks."""
@@ -781,9 +799,13 @@ def elementwise_workloads(c: Ctx) -> dict:
     z = c.pool.alloc_uninitialized(nd.float32, (n,))
     sig, op = "float a, float *x, float b, float *y, float *z", "z[i] = a * x[i] + b * y[i]"
     axes = dict(at.DEFAULT_AXES, waves=(0, 1, 2))
-    best = c.tune_on_rank0(lambda: at.tune_elementwise(
-        sig, op, "axpy", n, axes, args=[2.0, x, -3.0, y, z], protocol=c.proto, store=c.store,
-        burst=10).best_assignment)
+    def tune_axpy():
+        t = at.tune_elementwise(sig, op, "axpy", n, axes, args=[2.0, x, -3.0, y, z],
+                                protocol=c.proto, store=c.store, burst=10)
+        return confirm_best(c, t, lambda a: ew.ElementwiseKernel(sig, op, "axpy",
+                                                                 ew.VariantParams(**a)),
+                            lambda k: k(2.0, x, -3.0, y, z))
+    best = c.tune_on_rank0(tune_axpy)
     axpy = ew.ElementwiseKernel(sig, op, "axpy", ew.VariantParams(**best))
     with ClockSampler(c.bus_id) as clk:
         ms, _ = c.timed(lambda: axpy(2.0, x, -3.0, y, z), 10)
@@ -806,11 +828,21 @@ def elementwise_workloads(c: Ctx) -> dict:
     zd = c.pool.alloc_uninitialized(nd.float64, (n,))
     sig, op = ("double a, double *x, double *z",
                "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
-    ps_axes = dict(axes, waves=(0, 1, 2, 4), prefetch=(False, True))
-    best = c.tune_on_rank0(lambda: at.tune_elementwise(
-        sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
-        constraints=(lambda a: not a["prefetch"] or a["waves"] > 0,),
-        protocol=c.proto, store=c.store, burst=10).best_assignment)
+    # long statements: keep loads in flight through the arithmetic -- the
+    # register-pipelined loop (prefetch) or a per-thread cp.async ring (stages)
+    ps_axes = dict(unroll=(1, 2), block=(128, 256, 512, 1024), waves=(0, 1, 2, 4),
+                   prefetch=(False, True), stages=(0, 2, 3))
+
+    def tune_polysin():
+        t = at.tune_elementwise(
+            sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
+            constraints=(lambda a: not (a["prefetch"] or a["stages"]) or a["waves"] > 0,
+                         lambda a: not (a["prefetch"] and a["stages"])),
+            protocol=c.proto, store=c.store, burst=10)
+        return confirm_best(c, t, lambda a: ew.ElementwiseKernel(sig, op, "polysin",
+                                                                 ew.VariantParams(**a)),
+                            lambda k: k(0.5, xd, zd))
+    best = c.tune_on_rank0(tune_polysin)
     ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**best))
     with ClockSampler(c.bus_id) as clk:
         ms, _ = c.timed(lambda: ps(0.5, xd, zd), 10)

@@ -116,6 +116,37 @@ def tma_eligible(sig, access, width: int, block: int | None = None,
         return False
     return _tma_layout(sig, access, width, block, staged) is not None
 
+def async_eligible(sig, access, width: int) -> bool:
+    """A per-thread cp.async ring needs the vector path and a vector to read."""
+    return access is not None and width > 0 and any(access[p.name].read for p in sig.vectors)
+
+
+def async_parts(sig, access, width: int, stages: int, unroll: int, block: int) -> dict:
+    """Bindings of the elementwise vector path's cp.async ring (``stages``
+    steps of ``unroll`` chunks per read vector, ``block`` threads): ring
+    pointers into dynamic shared memory, the copy issue and the register
+    fetch per read vector, and the dynamic shared-memory size."""
+    rings, issue, issue_ahead, fetch = [], [], [], []
+    offset = 0
+    for p in sig.vectors:
+        if not access[p.name].read:
+            continue
+        c = p.dtype.cname
+        q = width * p.dtype.size // 16          # 16-byte words per chunk of this vector
+        rings.append(f"    int4 *rtcg_a_{p.name} = reinterpret_cast<int4 *>(rtcg_smem + {offset});")
+        slot = f"rtcg_a_{p.name} + ({{s}} * U + u) * {q * block}"
+        issue.append(f"                rtcg::async::issue<{c}, E, {block}>("
+                     f"{slot.format(s='s')}, rtcg_p_{p.name}, cu);")
+        issue_ahead.append(f"                    rtcg::async::issue<{c}, E, {block}>("
+                           f"{slot.format(s='sa')}, rtcg_p_{p.name}, cu);")
+        fetch.append(f"                rtcg::async::fetch<{c}, E, {block}>(rtcg_v_{p.name}[u], "
+                     f"{slot.format(s='s')});")
+        offset += stages * unroll * q * 16 * block
+    return {"stages": stages, "async_ring_decls": "\n".join(rings),
+            "async_issue": "\n".join(issue), "async_issue_ahead": "\n".join(issue_ahead),
+            "async_fetch": "\n".join(fetch), "async_smem": offset}
+
+
 _CONTROL = re.compile(r"\b(?:if|else|for|while|do|switch|case|goto|return|break|continue)\b|[{}]")
 
 
@@ -255,6 +286,7 @@ def parts(sig, access, width: int, policy: str) -> dict:
         "vec_loads_next": "\n".join(loads_next),
         "vec_copy_next": "\n".join(copies_next),
         "prefetch": False,
+        "stages": 0,
     }
 
 

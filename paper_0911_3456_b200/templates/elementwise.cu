@@ -61,6 +61,47 @@ ${vec_copy_next}
 ${vec_loads_next}
             }
         }
+{% endif %}{% if stages %}
+    // per-thread cp.async ring: each thread keeps its next S-1 steps of
+    // chunks in flight into its own shared-memory slots (no registers held,
+    // no barriers), so loads stay in flight through long statements
+    extern __shared__ __align__(16) unsigned char rtcg_smem[];
+${async_ring_decls}
+    constexpr int S = ${stages};
+    long c = tl.c_lo + sp.first;
+#pragma unroll
+    for (int s = 0; s < S - 1; ++s) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long cu = c + (s * U + u) * sp.step;
+            if (cu < tl.c_hi) {
+${async_issue}
+            }
+        }
+        rtcg::async::commit();
+    }
+    for (int s = 0; c < tl.c_hi; c += U * sp.step) {
+        {
+            const int sa = s == 0 ? S - 1 : s - 1;     // the slot read last step
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long cu = c + ((S - 1) * U + u) * sp.step;
+                if (cu < tl.c_hi) {
+${async_issue_ahead}
+                }
+            }
+            rtcg::async::commit();
+        }
+        rtcg::async::wait<S - 1>();                     // this step's copies landed
+${vec_decls}
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long cu = c + u * sp.step;
+            if (cu < tl.c_hi) {
+${async_fetch}
+            }
+        }
+        s = s + 1 == S ? 0 : s + 1;
 {% endif %}{% if no_prefetch %}
     for (long c = tl.c_lo + sp.first; c < tl.c_hi; c += U * sp.step) {
 ${vec_decls}

@@ -500,3 +500,54 @@ def test_double_sin_cos_within_two_ulp_of_glibc(kernel_env):
     ew.ElementwiseKernel("double *x, double *z", "z[i] = sin(x[i]) + cos(x[i])", "t_sc",
                          **kwargs)(special, out)
     assert np.all(np.isnan(out.to_host()))
+
+
+
+@pytest.mark.parametrize("stages, unroll, block", [(2, 1, 128), (3, 2, 256), (4, 1, 256),
+                                                   (8, 4, 64), (6, 1, 1024)])
+def test_cp_async_ring_matches_the_register_path(kernel_env, stages, unroll, block):
+    """``stages`` (per-thread cp.async ring) computes exactly what the plain
+    vector path computes: read-only, read-write and mixed-width vectors,
+    spans with unaligned heads/tails, shard bases, grids shorter than the
+    ring (tiny n) -- and the C oracle agrees."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(stages * 10 + unroll)
+    sig = "float a, float *x, double *y, double *z"
+    op = "z[i] += a * x[i] * y[i] - (double) i"
+    v_ring = ew.VariantParams(unroll=unroll, block=block, stages=stages, waves=1)
+    v_plain = ew.VariantParams(unroll=unroll, block=block, waves=1)
+    ring = ew.ElementwiseKernel(sig, op, "ring", v_ring, **kwargs)
+    plain = ew.ElementwiseKernel(sig, op, "plain", v_plain, **kwargs)
+    assert ring._async == (ring.smem > 0)
+    assert ("rtcg::async::issue" in ring.source) == ring._async
+    for n, lo in ((1 << 20, 0), (1_000_003, 3), (37, 1), (5, 0), (0, 0)):
+        x = rng.uniform(-1, 1, n + lo).astype(np.float32)
+        y = rng.uniform(-1, 1, n + lo)
+        z0 = rng.uniform(-1, 1, n + lo)
+        gx, gy = nd.from_host(pool, nd.float32, x), nd.from_host(pool, nd.float64, y)
+        outs = []
+        for k in (ring, plain):
+            gz = nd.from_host(pool, nd.float64, z0)
+            k(1.5, gx[lo:], gy[lo:], gz[lo:], base=7)
+            outs.append(gz.to_host())
+        assert outs[0].tobytes() == outs[1].tobytes(), (n, lo)
+        want = z0.copy()
+        cport.Elementwise(sig, op.replace("(double) i", "(double) (i + 7)"))(
+            1.5, np.ascontiguousarray(x[lo:]), np.ascontiguousarray(y[lo:]), want[lo:])
+        assert outs[0].tobytes() == want.tobytes(), (n, lo)
+
+
+def test_cp_async_ring_variant_validation():
+    with pytest.raises(ValueError):
+        ew.VariantParams(stages=5)
+    with pytest.raises(ValueError):
+        ew.VariantParams(stages=4, prefetch=True)
+    with pytest.raises(ValueError):
+        ew.VariantParams(stages=4, cache="tma")
+    # write-only statements have nothing to stage: the plain path is used
+    k = ew.ElementwiseKernel("float *z", "z[i] = 1.0f", "wo", ew.VariantParams(stages=4))
+    assert k.smem == 0 and not k._async and "cp.async.cg" not in k.source.split("end prelude")[1]
+    # a ring beyond the shared-memory budget falls back to the plain path
+    k = ew.ElementwiseKernel("float *x, double *y, double *z", "z[i] = x[i] * y[i]", "big",
+                             ew.VariantParams(stages=8, unroll=4, block=1024))
+    assert k.smem == 0 and not k._async
