@@ -363,8 +363,10 @@ def host_threads() -> int:
 
 def cpu_reference(x: np.ndarray, y: np.ndarray, warmup: int = 1, calls: int = 5) -> dict:
     """The reference's dot f32 on this host's cores, on the given arrays:
-    ``warmup`` calls, then the best of ``calls`` (BASELINE.md §3 protocol:
-    best-of-5 after one warm-up, ``time.perf_counter`` around one call).
+    ``warmup`` calls, then the best of ``calls`` (``time.perf_counter``
+    around one call, as BASELINE.md §3; both arms pass the bench's W and K,
+    so the GPU line's ``cpu_baseline`` and ``--impl reference`` measure the
+    same thing the same way).
 
     Stock ``rtcg.reduction.dot_kernel(float32)`` from ``baseline/_ref`` with
     the reference default variant (unroll 4, workers = cores, contiguous
@@ -1165,7 +1167,8 @@ def run_ours(args) -> int:
         cpu = None
         if d.world == 1 and d.rank == 0 and not args.no_cpu:
             try:
-                cpu = cpu_reference(h["hx"], h["hy"])
+                # the reference arm's protocol: W warm-up calls, best of K
+                cpu = cpu_reference(h["hx"], h["hy"], warmup=args.warmup, calls=args.steps)
             except Exception as exc:  # pragma: no cover - report, don't fail the bench
                 cpu = {"value": None, "error": str(exc)}
         for a in (h["gx"], h["gy"]):
