@@ -412,6 +412,51 @@ def cpu_reference(x: np.ndarray, y: np.ndarray, warmup: int = 1, calls: int = 5)
                       f"calls after {max(1, warmup)} warm-up"}
 
 
+CPU_SAMPLE = 1 << 26
+
+
+def stock_cpu(kind: str, arrays: list, nbytes: int, warmup: int = 1, calls: int = 5) -> dict:
+    """A secondary workload on the unmodified reference (``baseline/_ref``,
+    default variant, all host cores): ``arrays`` are host samples of the
+    GPU arm's own inputs; ``nbytes`` the algorithmic bytes of one call."""
+    stock = _stock_reference()
+    if stock is None:
+        return {"value": None, "error": "baseline/_ref not installed"}
+    rnd, rrd = stock
+    from rtcg import elementwise as rew
+    pool = rnd.MemoryPool()
+    dev = [rnd.from_host(pool, rnd.BY_NAME[a.dtype.name], a) for a in arrays]
+    if kind == "axpy":
+        k = rew.make_elementwise("float a, float *x, float b, float *y, float *z",
+                                 "z[i] = a * x[i] + b * y[i]", "axpy")
+        z = pool.alloc(rnd.float32, arrays[0].shape)
+
+        def call():
+            k(2.0, dev[0], -3.0, dev[1], z)
+    else:
+        k = {"maxabs": lambda: rrd.make_reduction("float *x", rnd.float32, "0",
+                                                  "a > b ? a : b", "fabsf(x[i])", "maxabs"),
+             "sumsq": lambda: rrd.make_reduction("float *x", rnd.float32, "0", "a + b",
+                                                 "x[i] * x[i]", "sumsq"),
+             "sum_i64": lambda: rrd.sum_kernel(rnd.int64)}[kind]()
+
+        def call():
+            return k(*dev)
+    for _ in range(max(1, warmup)):
+        call()
+    best = math.inf
+    for _ in range(max(1, calls)):
+        t0 = time.perf_counter()
+        call()
+        best = min(best, time.perf_counter() - t0)
+    n = arrays[0].size
+    return {"value": round(nbytes / best / 1e9, 3), "unit": "GB/s", "cores": os.cpu_count() or 1,
+            "kind": "reference",
+            "sample": f"{kind} n=2^{int(math.log2(n))} (bounded sample: the first elements of "
+                      f"the GPU arm's inputs), stock rtcg from baseline/_ref, default variant, "
+                      f"best of {max(1, calls)} after {max(1, warmup)} warm-up"}
+
+
 def run_reference(args) -> int:
     """CPU reference arm: rank 0 only, no GPU or process group needed."""
     if _env_int("RANK", 0) != 0:
@@ -721,6 +766,14 @@ def c4_workloads(c: Ctx) -> dict:
                      "frac": round(gbs / (c.peak * d.world), 4), "algorithmic_bytes": nbytes,
                      "n_total": N_C4, "n_per_gpu": m, "parity_ok": ok, "variant": tuned,
                      "launches_per_step": per, "note": note, "clocks": clk.summary(), **extra}
+        if d.world == 1 and not c.args.no_cpu:
+            sample = sx.local[:CPU_SAMPLE].to_host()
+            try:
+                out[name]["cpu_baseline"] = stock_cpu(
+                    name.split("_2p")[0].replace("_f32", ""), [sample],
+                    nbytes // N_C4 * sample.size, c.args.warmup, c.args.steps)
+            except Exception as exc:  # pragma: no cover - report, don't fail the bench
+                out[name]["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
 
     # max|x|: exact (max is order independent on NaN-free data)
     local_max = float(tf.abs().max().item())
@@ -820,6 +873,13 @@ def elementwise_workloads(c: Ctx) -> dict:
                             "frac": round(gbs / (c.peak * d.world), 4),
                             "algorithmic_bytes": 12 * n * d.world, "variant": best,
                             "parity_ok": ok, "clocks": clk.summary()}
+    if d.world == 1 and not c.args.no_cpu:
+        try:
+            out["axpy_f32_2p28"]["cpu_baseline"] = stock_cpu(
+                "axpy", [x[:CPU_SAMPLE].to_host(), y[:CPU_SAMPLE].to_host()],
+                12 * CPU_SAMPLE, c.args.warmup, c.args.steps)
+        except Exception as exc:  # pragma: no cover - report, don't fail the bench
+            out["axpy_f32_2p28"]["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
     del tx, ty, tz
     for a in (x, y, z):
         a.free()
