@@ -450,6 +450,8 @@ def stock_cpu(kind: str, arrays: list, nbytes: int, warmup: int = 1, calls: int 
         call()
         best = min(best, time.perf_counter() - t0)
     n = arrays[0].size
+    for a in dev + ([z] if kind == "axpy" else []):
+        a.free()
     return {"value": round(nbytes / best / 1e9, 3), "unit": "GB/s", "cores": os.cpu_count() or 1,
             "kind": "reference",
             "sample": f"{kind} n=2^{int(math.log2(n))} (bounded sample: the first elements of "

@@ -6,7 +6,7 @@ waves; reductions vector / general / TMA / combine / empty span / multi-CTA
 last-block fold; fused chains and fused chain+reduction; a captured graph;
 elementwise TMA rings (read, read-write, mixed widths, tile edges); the
 cross-rank peer exchange with emulated ranks on their own streams; views and
-streamed host calls (driver.In/Out).
+streamed host calls (driver.In/Out); per-thread cp.async rings.
 """
 import sys
 from pathlib import Path
@@ -62,6 +62,20 @@ for n in (1, 37, 20_000, 100_003):
     fusion.reduce(fusion.lazy(a) * 2 - a, "sum").get()
     a[n // 3:n // 2 + 1] * 2.0
     checks += 2
+# per-thread cp.async rings (stages): read-only, read-write, mixed widths,
+# unaligned heads/tails, grids shorter than the ring, shard bases
+for n in (1, 5, 37, 20_000, 100_003):
+    a = nd.from_host(pool, nd.float64, rng.uniform(-2, 2, n + 3))
+    f32 = nd.from_host(pool, nd.float32, rng.uniform(-1, 1, n + 3).astype(np.float32))
+    c = nd.from_host(pool, nd.float64, rng.uniform(-1, 1, n + 3))
+    for st, un, blk, wk in ((2, 1, 128, None), (3, 2, 256, None), (8, 4, 64, 2), (4, 1, 512, 1)):
+        rv = ew.VariantParams(stages=st, unroll=un, block=blk, waves=1, workers=wk)
+        ew.ElementwiseKernel("double a, double *x, double *z",
+                             "z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])", "rps", rv)(
+                                 0.5, a[1:], c[1:], base=5)
+        ew.ElementwiseKernel("float *x, double *y, double *z", "z[i] += x[i] * y[i]", "rmx", rv)(
+            f32, a, c, n=n)
+        checks += 2
 # peer exchange, 3 emulated ranks on their own streams (needs the ranks'
 # kernels to run concurrently: initcheck serialises launches, so it skips this)
 EXCHANGE = "--no-exchange" not in sys.argv
@@ -80,6 +94,16 @@ for st in streams:
 assert all(int(ks._read(ks.scratch(0, st.handle).result, nd.int64)) == int(xs.sum())
            for st in streams)
 checks += 9 if EXCHANGE else 0
+# a peer that never arrives: soft timeout, poisoned result, error word reported once
+lone = par.PeerMailbox.local_group(2, timeout_s=0.2)
+ks.launch(parts[0], peers=lone[0], out=pool.alloc(nd.int64, ()))
+try:
+    lone[0].check()
+    raise AssertionError("the missing peer was not reported")
+except par.PeerTimeout:
+    pass
+lone[0].check()
+checks += 1
 # overlapped (programmatic dependent) reductions back to back
 ov = rd.dot_kernel(nd.float32)
 oo = pool.alloc(nd.float32, ())
