@@ -36,8 +36,8 @@ ${unpack}
     const rtcg::span sp = rtcg::partition<rtcg::${chunking}>(start, end);
     const rtcg::tiles tl = rtcg::tile(sp.lo, sp.hi, E);
     auto elem = [&](const long i) { rtcg_op<${ptr_types_vector}>(i${call_args}); };
-    rtcg::for_each<1>(sp.lo + sp.first, tl.head_hi, sp.step, elem);
-    rtcg::for_each<1>(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
+    rtcg::for_edge(sp.lo + sp.first, tl.head_hi, sp.step, elem);
+    rtcg::for_edge(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
 {% if prefetch %}
     // software pipeline: the next step's chunks are loaded into registers
     // before this step's statement runs, so loads stay in flight during
@@ -173,8 +173,8 @@ ${ring_decls}
         rtcg::for_each<1>(start + gtid, end, gstep, elem);
         return;
     }
-    rtcg::for_each<1>(start + gtid, t_lo * TE, gstep, elem);
-    rtcg::for_each<1>(t_hi * TE + gtid, end, gstep, elem);
+    rtcg::for_edge(start + gtid, t_lo * TE, gstep, elem);
+    rtcg::for_edge(t_hi * TE + gtid, end, gstep, elem);
     const long mine = b < t_hi - t_lo ? (t_hi - t_lo - b + G - 1) / G : 0;
     if (warp == 0) {
         if (lane_id == 0) {

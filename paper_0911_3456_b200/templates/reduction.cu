@@ -81,8 +81,8 @@ ${ring_decls}
     if (t_lo >= t_hi) {
         rtcg::for_each<1>(start + gtid, end, gstep, elem);
     } else {
-        rtcg::for_each<1>(start + gtid, t_lo * TE, gstep, elem);
-        rtcg::for_each<1>(t_hi * TE + gtid, end, gstep, elem);
+        rtcg::for_edge(start + gtid, t_lo * TE, gstep, elem);
+        rtcg::for_edge(t_hi * TE + gtid, end, gstep, elem);
         const long mine = b < t_hi - t_lo ? (t_hi - t_lo - b + G - 1) / G : 0;
         if (warp == 0) {
             if (lane_id == 0) {
@@ -136,8 +136,8 @@ ${unpack}
     auto elem = [&](const long i) {
         acc = rtcg_fold(acc, rtcg_map<${ptr_types_vector}>(i${call_args}));
     };
-    rtcg::for_each<1>(sp.lo + sp.first, tl.head_hi, sp.step, elem);
-    rtcg::for_each<1>(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
+    rtcg::for_edge(sp.lo + sp.first, tl.head_hi, sp.step, elem);
+    rtcg::for_edge(tl.tail_lo + sp.first, sp.hi, sp.step, elem);
 {% if prefetch %}
     // software pipeline (prefetch=True): the next step's chunks are loaded
     // before this step's map/fold runs
