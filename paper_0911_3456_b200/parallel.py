@@ -367,6 +367,12 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
     previous kernel on the stream drains -- see ``ReductionKernel.launch``;
     with the exchange inside the kernel this also hides the previous step's
     exchange latency.
+
+    ``return_device=True`` returns the 0-d result without synchronising.  On
+    the p2p path a timed-out exchange leaves it poisoned (all bits set: NaN
+    / -1 / MAX), never this rank's partial value; call
+    ``peer_mailbox(group, stream).check(stream)`` to raise :class:`PeerTimeout`.
+    Host results (the default) are checked before they are returned.
     """
     import torch
     import torch.distributed as dist
