@@ -234,17 +234,63 @@ def reduce(expr, op: str = "sum", *, return_device: bool = True, stream=None):  
                   return_device=return_device, stream=stream)
 
 
+def _pure(fn) -> bool:
+    """Whether a traced function depends on nothing but its arguments: no
+    closure cells and no global names (literal constants only), so its trace
+    is a function of the arguments' dtypes, shapes and aliasing."""
+    code = getattr(fn, "__code__", None)
+    return code is not None and not getattr(fn, "__closure__", None) and not code.co_names
+
+
 def fused(fn, reduce: str | None = None):  # noqa: A002 - keyword mirrors the function
     """Decorator: ``fused(f)(*arrays)`` traces ``f`` over lazy leaves and
     evaluates it as one kernel; ``fused(f, reduce="sum")`` reduces the traced
-    chain in the same pass (a 0-d GPUArray)."""
+    chain in the same pass (a 0-d GPUArray).
+
+    When ``f`` is pure (see :func:`_pure`, e.g. ``lambda x, y: (x*2 + y) -
+    x``) and is called with GPUArrays only, the trace is kept per (dtypes,
+    shapes, aliasing) of the arguments: later calls skip the tracer and go
+    straight to the generated kernel (the same kernel, the same bits)."""
     reducer = reduce
+    cache = {} if _pure(fn) else None
+
+    def trace(args):
+        return fn(*(Expr(("A", a), a.dtype, a.shape) if a.__class__ is NdArray else
+                    lazy(a) if isinstance(a, NdArray) else a for a in args))
 
     def run(*args, out=None, stream=None):
-        traced = fn(*(Expr(("A", a), a.dtype, a.shape) if a.__class__ is NdArray else
-                      lazy(a) if isinstance(a, NdArray) else a for a in args))
+        key = None
+        if cache is not None and args and all(a.__class__ is NdArray for a in args):
+            ids = [id(a) for a in args]
+            key = (tuple((a.dtype.name, a.shape) for a in args),
+                   tuple(ids.index(i) for i in ids))
+            hit = cache.get(key)
+            if hit is not None:
+                run.cache_hits += 1
+                kernel, positions, values, dtype, shape = hit
+                arrays = [args[p] for p in positions]
+                if reducer is not None:
+                    return kernel(*arrays, *values, n=arrays[0].size, return_device=True,
+                                  stream=stream)
+                if out is None:
+                    out = arrays[0].pool.alloc_uninitialized(dtype, shape)
+                elif out.dtype != dtype or out.shape != shape:
+                    raise ShapeMismatch("out does not match the expression's dtype/shape")
+                kernel(*arrays, *values, out, n=out.size, stream=stream)
+                return out
+        traced = trace(args)
+        if key is not None and isinstance(traced, Expr):
+            skey, arrays, scalars = traced._leaves()
+            if reducer is not None:
+                kernel = _reduction_for(skey, arrays, scalars, traced.dtype, reducer)
+            else:
+                kernel = _kernel_for(skey, arrays, scalars, traced.dtype)
+            positions = tuple(next(k for k, a in enumerate(args) if a is leaf) for leaf in arrays)
+            cache[key] = (kernel, positions, tuple(v for v, _ in scalars), traced.dtype,
+                          traced.shape)
         if reducer is not None:
             return globals()["reduce"](traced, reducer, stream=stream)
         return evaluate(traced, out=out, stream=stream)
     run.__name__ = getattr(fn, "__name__", "fused")
+    run.cache_hits = 0
     return run

@@ -218,3 +218,40 @@ def test_fused_reductions_equal_the_oracle(pool, dname):
             assert abs(float(got) - float(want)) <= 2 * csem.float_reduction_bound(terms, dname)
         else:
             assert got.tobytes() == np.asarray(want).tobytes(), (op, got, want)
+
+
+@pytest.mark.gpu
+def test_fused_trace_cache_is_keyed_by_dtypes_shapes_and_aliasing(pool):
+    """A pure chain is traced once per argument signature; hits run the same
+    kernel on the new arrays and give the uncached bits."""
+    rng = np.random.default_rng(21)
+    h = [rng.uniform(-2, 2, 4099).astype(np.float32) for _ in range(3)]
+    x, y, w = (nd.from_host(pool, nd.float32, a) for a in h)
+    f = fusion.fused(lambda p, q: (p * 2 + q) - p)
+    first = f(x, y).get()
+    assert f.cache_hits == 0
+    again = f(w, y).get()                       # same signature, new arrays: a hit
+    assert f.cache_hits == 1
+    assert first.tobytes() == (och.HostArray(h[0]) * 2 + och.HostArray(h[1]) -
+                               och.HostArray(h[0])).values.tobytes()
+    assert again.tobytes() == (och.HostArray(h[2]) * 2 + och.HostArray(h[1]) -
+                               och.HostArray(h[2])).values.tobytes()
+    aliased = f(x, x).get()                     # aliasing changes the trace: a miss
+    assert f.cache_hits == 1
+    assert aliased.tobytes() == (och.HostArray(h[0]) * 2 + och.HostArray(h[0]) -
+                                 och.HostArray(h[0])).values.tobytes()
+    xd = nd.from_host(pool, nd.float64, h[0].astype(np.float64))
+    assert f(xd, y).dtype is nd.float64 and f.cache_hits == 1     # new dtypes: a miss
+    out = pool.alloc(nd.float32, (4099,))
+    assert f(w, y, out=out) is out and f.cache_hits == 2
+    assert out.get().tobytes() == again.tobytes()
+    with pytest.raises(nd.ShapeMismatch):
+        f(w, y, out=pool.alloc(nd.float64, (4099,)))
+    r = fusion.fused(lambda p, q: p * q + 1, reduce="max")
+    want = np.max(h[0] * h[1] + np.float32(1))
+    assert r(x, y).get() == want and r(x, y).get() == want and r.cache_hits == 1
+    scale = [2.0]
+    g = fusion.fused(lambda p: p * scale[0])    # a closure: never cached
+    g(x)
+    scale[0] = 3.0
+    assert np.array_equal(g(x).get(), h[0].astype(np.float64) * 3.0) and g.cache_hits == 0
