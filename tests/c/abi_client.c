@@ -86,9 +86,23 @@ int main(int argc, char **argv) {
     double wa = 2.0, wb = -3.0;
     long start = 0, end = n;
     void *params[] = {&wa, &dx, &wb, &dy, &dz, &start, &end};
-    CHECK(rtcg_launch(fn, 592, 256, 0, NULL, params));
-    CHECK(rtcg_copy_dtoh(hz, dz, bytes, NULL));
-    CHECK(rtcg_synchronize());
+    /* launch on a private stream ordered after the uploads on the legacy
+     * stream (what the streamed host calls do with the caller's stream) */
+    rtcg_stream_t stream;
+    rtcg_event_t uploaded;
+    CHECK(rtcg_stream_create(&stream));
+    CHECK(rtcg_event_create(&uploaded));
+    CHECK(rtcg_event_record(uploaded, NULL));
+    CHECK(rtcg_stream_wait_event(stream, uploaded));
+    CHECK(rtcg_launch(fn, 592, 256, 0, stream, params));
+    CHECK(rtcg_copy_dtoh(hz, dz, bytes, stream));
+    CHECK(rtcg_stream_synchronize(stream));
+    CHECK(rtcg_event_destroy(uploaded));
+    CHECK(rtcg_stream_destroy(stream));
+    char bus[32];
+    CHECK(rtcg_device_pci_bus_id(0, bus, (int) sizeof bus));
+    if (rtcg_device_pci_bus_id(0, bus, 4) != RTCG_ERR_INVALID) return 7;
+    printf("device 0 at %s\n", bus);
     long bad_count = 0;
     for (long i = 0; i < n; ++i) {
         volatile float ax = 2.0f * hx[i], by = -3.0f * hy[i];   /* no contraction */

@@ -96,3 +96,4 @@ def test_c_client_launches_through_the_abi(tmp_path):
                          text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "0 mismatches" in out.stdout
+    assert re.search(r"device 0 at [0-9a-fA-F]{4,8}:[0-9a-fA-F]{2}:", out.stdout), out.stdout
