@@ -29,7 +29,11 @@ def stock_sources(variant: ew.VariantParams | None = None) -> dict:
     variant = variant or ew.VariantParams()
     out = {}
     for name, (sig, op) in ELEMENTWISE.items():
-        out[name] = ew.generate(ew.parse_signature(sig), op, name, variant)
+        # what ElementwiseKernel compiles: the vector entry eagerly, the
+        # general entry on first need
+        out[name] = ew.generate(ew.parse_signature(sig), op, name, variant, entries="vector")
+        out[f"{name}_g"] = ew.generate(ew.parse_signature(sig), op, name, variant,
+                                       entries="general")
     for name, (sig, dt, neutral, red, mp) in REDUCTIONS.items():
         out[name] = rd.generate_reduction_source(rd.ReductionSpec(sig, dt, neutral, red, mp),
                                                  name, variant)

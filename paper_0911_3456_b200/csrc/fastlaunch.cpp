@@ -47,7 +47,7 @@ struct Plan {
     PyObject *owners;          // keeps dtype objects / array type alive
     PyTypeObject *array_type;
     Entry vec, gen;
-    bool has_vec;
+    bool has_vec, has_gen;
     unsigned block;
     long long workers;         // 0 = policy
     int nextra;
@@ -74,7 +74,7 @@ bool read_entry(PyObject *t, Entry &e) {
     return true;
 }
 
-// Plan(params, array_type, block, workers, gen_entry, vec_entry_or_None, nextra)
+// Plan(params, array_type, block, workers, gen_entry_or_None, vec_entry_or_None, nextra)
 // params: sequence of (is_vector, dtype, itemsize, kind, used, written)
 int plan_init(Plan *self, PyObject *args, PyObject *) {
     PyObject *params, *array_type, *gen, *vec;
@@ -114,7 +114,8 @@ int plan_init(Plan *self, PyObject *args, PyObject *) {
     self->block = block;
     self->workers = workers;
     self->nextra = nextra;
-    if (!read_entry(gen, self->gen)) return -1;
+    self->has_gen = gen != Py_None;
+    if (self->has_gen && !read_entry(gen, self->gen)) return -1;
     self->has_vec = vec != Py_None;
     if (self->has_vec && !read_entry(vec, self->vec)) return -1;
     return 0;
@@ -253,6 +254,7 @@ PyObject *plan_launch(Plan *self, PyObject *const *argv, Py_ssize_t argc) {
             if (lo_a < hi_b && lo_b < hi_a) { vec_ok = false; break; }
         }
     }
+    if (!vec_ok && !self->has_gen) Py_RETURN_NONE;   // general entry not built yet
     const Entry &e = vec_ok ? self->vec : self->gen;
     const long long grid = grid_of(self, e, n);
     if (max_grid >= 0 && grid > max_grid) Py_RETURN_NONE;

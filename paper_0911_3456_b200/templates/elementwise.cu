@@ -11,6 +11,7 @@ __device__ __forceinline__ void rtcg_op(const long i${op_params})
 ${operation}
 }
 
+{% if general %}
 // General path: any statement over the parameters, one element per thread
 // per step, ${unroll} statements in flight.
 extern "C" __global__ void __launch_bounds__(${block})
@@ -22,6 +23,7 @@ ${unpack}
         rtcg_op<${ptr_types_generic}>(i${call_args});
     });
 }
+{% endif %}
 {% if vector %}
 // Vector path: every vector is used only as name[i], all index-0 addresses
 // are 16-byte aligned and no written vector aliases another.  Each thread

@@ -551,3 +551,30 @@ def test_cp_async_ring_variant_validation():
     k = ew.ElementwiseKernel("float *x, double *y, double *z", "z[i] = x[i] * y[i]", "big",
                              ew.VariantParams(stages=8, unroll=4, block=1024))
     assert k.smem == 0 and not k._async
+
+
+def test_general_entry_is_compiled_on_first_need(kernel_env, tmp_path):
+    """Construction runs NVRTC once (the vector entry); aligned calls never
+    build the general entry; a misaligned view builds it once, runs it
+    correctly, and later misaligned calls go through the native plan."""
+    from paper_0911_3456_b200 import jit
+    kwargs, pool = kernel_env
+    cache = jit.CacheStore(tmp_path / "lazy-cache")
+    before = jit.compiler_spawn_count()
+    k = ew.ElementwiseKernel("float a, float *x, float *z", "z[i] = a * x[i] + 1.0f",
+                             "lazy_g", cache=cache, config=kwargs["config"])
+    assert jit.compiler_spawn_count() - before == 1
+    assert not k.generic.ready and "lazy_g_g(" not in k.source
+    n = 100_003
+    host = np.random.default_rng(2).uniform(-1, 1, n + 1).astype(np.float32)
+    x, z = nd.from_host(pool, nd.float32, host), pool.alloc(nd.float32, (n + 1,))
+    k(2.0, x, z)
+    assert jit.compiler_spawn_count() - before == 1 and not k.generic.ready
+    z2 = pool.alloc(nd.float32, (n,))
+    k(2.0, x[1:], z2)                                   # 4-byte offset: general path
+    assert k.generic.ready and jit.compiler_spawn_count() - before == 2
+    assert np.array_equal(z2.get(), np.float32(2.0) * host[1:] + np.float32(1.0))
+    assert np.array_equal(z.get(), np.float32(2.0) * host + np.float32(1.0))
+    k(2.0, x[1:], z2)
+    assert jit.compiler_spawn_count() - before == 2
+    assert k.launch_config(2.0, x[1:], z2)["entry"] == "lazy_g_g"
