@@ -35,8 +35,9 @@ def stock_sources(variant: ew.VariantParams | None = None) -> dict:
         out[f"{name}_g"] = ew.generate(ew.parse_signature(sig), op, name, variant,
                                        entries="general")
     for name, (sig, dt, neutral, red, mp) in REDUCTIONS.items():
-        out[name] = rd.generate_reduction_source(rd.ReductionSpec(sig, dt, neutral, red, mp),
-                                                 name, variant)
+        spec = rd.ReductionSpec(sig, dt, neutral, red, mp)
+        out[name] = rd.generate_reduction_source(spec, name, variant, entries="vector")
+        out[f"{name}_g"] = rd.generate_reduction_source(spec, name, variant, entries="general")
     return out
 
 

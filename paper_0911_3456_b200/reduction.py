@@ -42,7 +42,7 @@ from . import jit
 from . import ndarray as nd
 from .driver import HostArg as _HostArg, In as _In, InOut as _InOut, Out as _Out
 from .elementwise import (_CHUNK_TOKEN, _ERRORS, ArityMismatch, DtypeMismatch, KernelSignature,
-                          ParseError, VariantParams, _check_name, _preamble_text,
+                          ParseError, VariantParams, _check_name, _LazyEntry, _preamble_text,
                           parse_signature)
 from .ndarray import Dtype
 
@@ -101,9 +101,14 @@ class ReductionSpec:
 
 
 def generate_reduction_source(spec: ReductionSpec, name: str,
-                              variant: VariantParams, preamble: str = "") -> str:
+                              variant: VariantParams, preamble: str = "",
+                              entries: str = "all") -> str:
     """CUDA source with ``<name>`` (vector path, when legal), ``<name>_g``
-    (general) and ``<name>_combine`` (ordered fold of partials)."""
+    (general) and ``<name>_combine`` (ordered fold of partials).
+    ``entries``: "all", "vector" (``<name>`` + ``<name>_combine``) or
+    "general" (``<name>_g`` only)."""
+    if entries not in ("all", "vector", "general"):
+        raise ValueError(f"entries must be 'all', 'vector' or 'general', got {entries!r}")
     _check_name(name)
     sig = spec.signature
     access = cg.analyze(spec.mapped, [p.name for p in sig.vectors])
@@ -114,6 +119,9 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
     if variant.cache == "tma" and b["vector"]:
         b.update(cg.tma_parts(sig, access, width))
         b["vector"] = False  # the TMA entry point takes the vector path's name
+    if entries == "general":
+        b.update(vector=False, tma=False)
+    b.update(general=entries != "vector", combine=entries != "general")
     b["map_tparams"] = b.pop("op_tparams")
     b["map_params"] = b.pop("op_params")
     b.update(name=name, unroll=variant.unroll, block=variant.block,
@@ -201,16 +209,30 @@ class ReductionKernel:
         self.name = name
         self.variant = (variant or VariantParams()).resolved()
         self.return_device = False
-        self.source = generate_reduction_source(spec, name, self.variant, preamble)
         sig = spec.signature
         access = cg.analyze(spec.mapped, [p.name for p in sig.vectors])
         if access is not None and any(a.written for a in access.values()):
             access = None
         self.access = access
         self.width = cg.chunk_width(sig, access) if access is not None else 0
-        self.module = jit.compile(self.source, config, cache)
-        self.generic = jit.get_kernel(self.module, f"{name}_g")
-        self.vectorized = jit.get_kernel(self.module, name) if self.access and self.width else None
+        self._plans: dict = {}
+        if self.access and self.width:
+            # vector (or TMA) entry + combine now; the general entry point
+            # (misaligned / aliased arguments) on first need
+            self.source = generate_reduction_source(spec, name, self.variant, preamble,
+                                                    entries="vector")
+            self.module = jit.compile(self.source, config, cache)
+            self.vectorized = jit.get_kernel(self.module, name)
+            self.generic = _LazyEntry(
+                f"{name}_g", lambda: jit.compile(
+                    generate_reduction_source(spec, name, self.variant, preamble,
+                                              entries="general"), config, cache),
+                self._plans.clear)
+        else:
+            self.source = generate_reduction_source(spec, name, self.variant, preamble)
+            self.module = jit.compile(self.source, config, cache)
+            self.vectorized = None
+            self.generic = jit.get_kernel(self.module, f"{name}_g")
         self.smem = 0
         self._tma_tile = 0
         if self.vectorized is not None and self.variant.cache == "tma":
@@ -223,7 +245,6 @@ class ReductionKernel:
         self._binder = cg.Binder(sig, extra=6)
         self._waves = 1 if self.variant.waves is None else self.variant.waves
         self._scratch: dict[int, _Scratch] = {}
-        self._plans: dict = {}
         self._lock = threading.Lock()
         self.launches = 0
         if debug:
@@ -302,9 +323,11 @@ class ReductionKernel:
             return plan
         sms = cg.sm_count(dev)
         block = self.variant.block
-        gen_fn = self.generic.function(dev)
-        gen = (gen_fn, self.variant.unroll, sms * max(1, _runtime.occupancy(gen_fn, block, 0)),
-               self._waves, 0)
+        gen = None              # not compiled yet: calls that need it take the Python path
+        if not isinstance(self.generic, _LazyEntry) or self.generic.ready:
+            gen_fn = self.generic.function(dev)
+            gen = (gen_fn, self.variant.unroll,
+                   sms * max(1, _runtime.occupancy(gen_fn, block, 0)), self._waves, 0)
         vec = None
         if self.vectorized is not None:
             fn = self.vectorized.function(dev)

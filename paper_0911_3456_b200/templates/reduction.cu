@@ -20,6 +20,7 @@ __device__ __forceinline__ auto rtcg_map(const long i${map_params})
 
 #define RTCG_NEUTRAL ((${acc_t})(${neutral}))
 
+{% if general %}
 // General path: thread-serial folds in index order, then lanes -> warps ->
 // CTA partial, then the last CTA folds the partials in CTA order.
 extern "C" __global__ void __launch_bounds__(${block})
@@ -37,6 +38,7 @@ ${unpack}
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
                  [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
 }
+{% endif %}
 {% if tma %}
 // TMA path: a producer warp streams ${stages} ring stages of ${tile}-element
 // tiles of every input into shared memory with 1-D bulk copies (cp.async.bulk,
@@ -185,6 +187,7 @@ ${vec_loads}
                  [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
 }
 {% endif %}
+{% if combine %}
 // Ordered fold of partials[start, end) from the neutral into result[0]; the
 // reference's <name>_combine entry point (src/reduction.py:154-168).  Used for
 // empty spans, the neutral probe and the cross-GPU combine of rank partials.
@@ -197,3 +200,4 @@ extern "C" __global__ void ${name}_combine(const ${acc_t} *rtcg_in, ${acc_t} *rt
     rtcg_result[0] = acc;
     rtcg_out[0] = (${out_t})acc;
 }
+{% endif %}

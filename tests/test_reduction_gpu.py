@@ -319,3 +319,23 @@ def test_overlapped_launches_give_the_same_results(kernel_env):
     for _ in range(10):
         general.launch(x, out=og, overlap_previous=True)
     assert float(og.get()) == float(general(x))
+
+
+def test_reduction_general_entry_is_compiled_on_first_need(kernel_env, tmp_path):
+    """A reduction builds its vector entry and combine at construction, the
+    general entry only when a call needs it (misaligned view), and both give
+    the same fold."""
+    from paper_0911_3456_b200 import jit
+    kwargs, pool = kernel_env
+    cache = jit.CacheStore(tmp_path / "lazy-red")
+    before = jit.compiler_spawn_count()
+    k = rd.sum_kernel(nd.int64, cache=cache, config=kwargs["config"])
+    assert jit.compiler_spawn_count() - before == 1 and not k.generic.ready
+    host = np.arange(100_001, dtype=np.int64)
+    x = nd.from_host(pool, nd.int64, host)
+    assert int(k(x)) == int(host.sum()) and not k.generic.ready
+    assert int(k(x, n=0)) == 0 and not k.generic.ready          # empty span: the combine
+    assert int(k(x[1:])) == int(host[1:].sum())                  # 8-byte offset: general
+    assert k.generic.ready and jit.compiler_spawn_count() - before == 2
+    assert int(k(x[1:])) == int(host[1:].sum())
+    assert jit.compiler_spawn_count() - before == 2
