@@ -153,8 +153,8 @@ _NCCL_DTYPES = {"int8", "uint8", "int32", "int64", "float32", "float64"}
 # --- peer-memory exchange (the fused cross-GPU combine) -------------------------------------
 
 XR_MAX = 64                             # rtcg::XR_MAX in templates/prelude.cuh
-XR_ERROR = 3 * XR_MAX                   # rtcg::XR_ERROR: epoch of a timed-out wait
-MAILBOX_BYTES = 8 * (3 * XR_MAX + 8)    # epoch flags, two accumulator banks, error word
+XR_ERROR = 4 * XR_MAX                   # rtcg::XR_ERROR: epoch of a timed-out wait
+MAILBOX_BYTES = 8 * (4 * XR_MAX + 8)    # two banks x 64 tagged 2-word slots, error word
 _XR = struct.Struct(f"<ii{XR_MAX}QQ")    # struct rtcg::xr {int rank, world; u64 mbox[64], timeout_ns;}
 DEFAULT_TIMEOUT_S = 20.0
 

@@ -1,7 +1,6 @@
 """ncu probe of the peer exchange's device cost at world size 1: dot f32
-launches local vs with a one-rank mailbox, for exchange protocol variants
-(-DRTCG_XR_PROTOCOL=0: fence.sc.sys + acquire polls; 1: fence.acq_rel.sys
-on both sides, relaxed polls; 2: no fences -- timing reference only)."""
+launches local vs with a one-rank mailbox (run under ncu -k regex:dot_p;
+profiles/r02_probe_p2p_ncu.json holds the protocol history)."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -16,8 +15,8 @@ for lg in (20, 28):
     x = nd.from_host(pool, nd.float32, np.ones(n, np.float32))
     y = nd.from_host(pool, nd.float32, np.ones(n, np.float32))
     o = pool.alloc_uninitialized(nd.float32, ())
-    for proto in (0, 1, 2, 3):
-        cfg = jit.ToolchainConfig(flags=jit.DEFAULT_FLAGS + (f"-DRTCG_XR_PROTOCOL={proto}",))
+    for proto in (0,):
+        cfg = jit.ToolchainConfig()
         k = rd.ReductionKernel(rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b",
                                                 "x[i] * y[i]"), f"dot_p{proto}",
                                ew.VariantParams(block=256, unroll=1, waves=2), config=cfg)
