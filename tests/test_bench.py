@@ -13,9 +13,11 @@ BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_ste
              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
 
 
-def _run(*args, timeout=600):
+def _run(*args, timeout=600, env=None):
+    import os
     proc = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], cwd=ROOT,
-                          capture_output=True, text=True, timeout=timeout)
+                          capture_output=True, text=True, timeout=timeout,
+                          env=None if env is None else dict(os.environ, **env))
     assert proc.returncode == 0, proc.stderr[-2000:]
     lines = [ln for ln in proc.stdout.splitlines() if ln.strip()]
     assert len(lines) == 1, proc.stdout
@@ -125,3 +127,15 @@ def test_workload_config_is_shared_by_both_arms():
     import bench
     assert bench.workload_config(1)["n_total"] == 1 << 28
     assert bench.workload_config(8)["n_total"] == 8 << 28
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_processes_through_the_peer_exchange():
+    """The product path across processes: two ranks on the one B200 exchange
+    their accumulators inside the reduction kernel through CUDA IPC-mapped
+    mailboxes (what NVLink peers do on an 8-GPU box), parity-checked."""
+    line = _run("--gpus", "2", "--steps", "5", "--warmup", "3", "--quick", "--no-cpu",
+                env={"RTCG_BENCH_COLLECTIVE": "p2p"})
+    assert line["n_ranks_seen"] == 2 and line["collective"] == "p2p"
+    assert line["parity_ok"] is True and line["parity"]["dot_ranks_agree"] is True
+    assert line["gpu_launches"] == 5          # one kernel per step: the exchange is inside
