@@ -939,9 +939,13 @@ def elementwise_workloads(c: Ctx) -> dict:
             sig, op, "polysin", n, ps_axes, args=[0.5, xd, zd],
             constraints=(lambda a: not (a["prefetch"] and a["stages"]),),
             protocol=c.proto, store=c.store, burst=10)
+        # confirmed over 100-launch bursts: at full HBM bandwidth this FP64
+        # statement holds the board at its 1000 W cap (SM clock ~1.6 GHz), and
+        # the variants rank differently there than in short bursts
+        # (profiles/r02_polysin_sustained.json)
         return confirm_best(c, t, lambda a: ew.ElementwiseKernel(sig, op, "polysin",
                                                                  ew.VariantParams(**a)),
-                            lambda k: k(0.5, xd, zd))
+                            lambda k: k(0.5, xd, zd), burst=100)
     best = c.tune_on_rank0(tune_polysin)
     ps = ew.ElementwiseKernel(sig, op, "polysin", ew.VariantParams(**best))
     with ClockSampler(c.bus_id) as clk:

@@ -48,7 +48,7 @@ def time_ms(k, x, z, burst=10, reps=3):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("mode", choices=("sweep", "one", "ops"))
+    p.add_argument("mode", choices=("sweep", "one", "ops", "sustained"))
     p.add_argument("variant", nargs="?", default="{}")
     p.add_argument("--fma", action="store_true")
     p.add_argument("--op", default=OP)
@@ -63,6 +63,23 @@ def main():
     x = nd.from_host(pool, nd.float64, np.random.default_rng(1).uniform(-2, 2, N))
     z = pool.alloc_uninitialized(nd.float64, (N,))
     pre = Path(a.preamble).read_text() if a.preamble else ""
+    if a.mode == "sustained":   # variants under the board's power cap: heat, then long bursts
+        rows = []
+        variants = json.loads(a.variants)
+        ks = [kernel(v, a.fma, a.op, pre) for v in variants]
+        heat = ks[0]
+        for _ in range(3000):          # ~2 s of the workload itself
+            heat(0.5, x, z)
+        rt.synchronize()
+        for rnd in range(2):
+            for v, k in zip(variants, ks):
+                ms = time_ms(k, x, z, burst=100, reps=2)
+                row = {**v, "round": rnd, "us": round(ms * 1e3, 1),
+                       "GB/s": round(16 * N / ms / 1e6, 1)}
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+        Path(a.out).write_text(json.dumps(rows, indent=1))
+        return
     if a.mode == "ops":       # every op line x every variant, same process
         rows = []
         for line in Path(a.ops).read_text().splitlines():
