@@ -139,3 +139,27 @@ def test_gpu_arm_two_processes_through_the_peer_exchange():
     assert line["n_ranks_seen"] == 2 and line["collective"] == "p2p"
     assert line["parity_ok"] is True and line["parity"]["dot_ranks_agree"] is True
     assert line["gpu_launches"] == 5          # one kernel per step: the exchange is inside
+
+
+def test_roofline_traffic_is_looked_up_for_the_timed_variant():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    table_hit = bench._ncu_traffic("dot_k", {"block": 128, "unroll": 1, "waves": 2})
+    assert table_hit[2] is True and table_hit[1] == {"block": 128, "unroll": 1, "waves": 2}
+    assert 0.99 < table_hit[0] / (8 << 28) < 1.01
+    # variant keys ignore absent-vs-default spelling
+    assert bench._variant_key({"block": 256}) == bench._variant_key(
+        {"block": 256, "cache": "default", "unroll": 1, "waves": 1})
+    assert bench._ncu_traffic("no_such_kernel", {}) == (None, None, False, None)
+
+
+def test_reduction_check_bound_and_bit_equality():
+    from fractions import Fraction
+    sys.path.insert(0, str(ROOT))
+    import bench
+    exact = Fraction(1, 3)
+    got = float(exact)                               # fp64 rounding of 1/3
+    chk = bench.reduction_check(got, exact, n=4, sum_abs=1.0)
+    assert chk["ok"] and chk["bit_equal_f32_fsum"] and chk["ulps"] < 1e-6
+    far = bench.reduction_check(got + 1e-3, exact, n=4, sum_abs=1.0)
+    assert not far["ok"] and not far["bit_equal_f32_fsum"]
