@@ -282,3 +282,13 @@ def test_peer_descriptor_layout_matches_prelude(nvrtc_cache):
            + '\nextern "C" __global__ void layout_probe() {}\n')
     jit.compile(src, cache=nvrtc_cache)
     assert par.MAILBOX_BYTES >= 8 * (par.XR_ERROR + 1)
+
+
+def test_default_variant_pipelines_transcendental_statements():
+    """Untuned statements that call transcendentals get the register-
+    pipelined loop (r02_probe_heavy_defaults.json); others the plain one."""
+    heavy = ew.default_variant("z[i] = ((a*x[i] + 2.0)*x[i] - 1.5)*x[i] + sin(x[i])")
+    assert heavy.prefetch and heavy.waves == 4
+    assert ew.default_variant("z[i] = expf (x[i])").prefetch
+    assert ew.default_variant("z[i] = a * x[i] + sinus[i]") == ew.VariantParams()
+    assert ew.default_variant("z[i] = x[i] + y[i]") == ew.VariantParams()
