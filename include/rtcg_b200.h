@@ -169,6 +169,10 @@ int rtcg_event_record(rtcg_event_t event, rtcg_stream_t stream);
 /* Work submitted to `stream` after this call waits for `event` (cuStreamWaitEvent);
  * streamed host calls order their private streams after the caller's stream. */
 int rtcg_stream_wait_event(rtcg_stream_t stream, rtcg_event_t event);
+/* *capturing = 1 while `stream` is being captured into a CUDA graph
+ * (cuStreamIsCapturing): overlapped reductions fall back to their serial
+ * scratch slot there, since a replay re-runs baked launch numbers. */
+int rtcg_stream_is_capturing(rtcg_stream_t stream, int *capturing);
 int rtcg_event_synchronize(rtcg_event_t event);
 int rtcg_event_elapsed_ms(rtcg_event_t start, rtcg_event_t end, float *ms);
 

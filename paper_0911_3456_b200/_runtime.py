@@ -151,6 +151,7 @@ _PROTOTYPES = {
     "rtcg_event_record": (_vp, _vp),
     "rtcg_device_pci_bus_id": (_int, ctypes.c_char_p, _int),
     "rtcg_stream_wait_event": (_vp, _vp),
+    "rtcg_stream_is_capturing": (_vp, _pint),
     "rtcg_event_synchronize": (_vp,),
     "rtcg_event_elapsed_ms": (_vp, _vp, ctypes.POINTER(ctypes.c_float)),
     "rtcg_stream_begin_capture": (_vp,),
@@ -424,6 +425,15 @@ def stream_wait_event(stream, event: Event) -> None:
     """Work submitted to ``stream`` (raw handle, 0 = legacy) after this call
     waits for ``event`` (cuStreamWaitEvent)."""
     _check(lib().rtcg_stream_wait_event(stream or None, event.handle), "stream wait event")
+
+
+def stream_is_capturing(stream=None) -> bool:
+    """Whether ``stream`` (default: this thread's current stream) is being
+    captured into a CUDA graph."""
+    s = current_stream() if stream is None else getattr(stream, "handle", stream)
+    out = ctypes.c_int()
+    _check(lib().rtcg_stream_is_capturing(s or None, ctypes.byref(out)), "is capturing")
+    return bool(out.value)
 
 
 def order_after_current(streams) -> None:

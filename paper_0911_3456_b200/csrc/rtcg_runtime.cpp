@@ -101,6 +101,7 @@ struct Driver {
     X(cuStreamDestroy_v2, CUresult(CUstream))                              \
     X(cuStreamSynchronize, CUresult(CUstream))                             \
     X(cuStreamWaitEvent, CUresult(CUstream, CUevent, unsigned))            \
+    X(cuStreamIsCapturing, CUresult(CUstream, CUstreamCaptureStatus *))     \
     X(cuEventCreate, CUresult(CUevent *, unsigned))                        \
     X(cuEventDestroy_v2, CUresult(CUevent))                                \
     X(cuEventRecord, CUresult(CUevent, CUstream))                          \
@@ -941,6 +942,16 @@ int rtcg_stream_wait_event(rtcg_stream_t stream, rtcg_event_t event) {
     CU_CALL(g_drv.cuStreamWaitEvent(reinterpret_cast<CUstream>(stream),
                                     reinterpret_cast<CUevent>(event), 0),
             "cuStreamWaitEvent");
+    return RTCG_OK;
+}
+
+int rtcg_stream_is_capturing(rtcg_stream_t stream, int *capturing) {
+    NEED_CONTEXT();
+    if (!capturing) return fail(RTCG_ERR_INVALID, "null capturing");
+    CUstreamCaptureStatus st = CU_STREAM_CAPTURE_STATUS_NONE;
+    CU_CALL(g_drv.cuStreamIsCapturing(reinterpret_cast<CUstream>(stream), &st),
+            "cuStreamIsCapturing");
+    *capturing = st != CU_STREAM_CAPTURE_STATUS_NONE;
     return RTCG_OK;
 }
 

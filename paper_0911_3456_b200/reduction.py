@@ -132,12 +132,23 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
     return cg.render("reduction.cu", b)
 
 
+_SERIAL = 1 << 63
+
+
 class _Scratch:
-    """Per-device partials / result / out / ticket buffers of one kernel."""
+    """Per-device partials / result / out / ticket buffers of one kernel.
+
+    Three partials regions of ``capacity`` accumulators: two alternate
+    between overlapped launches (so a launch's CTAs may publish while the
+    previous launch still folds the other region) and one serves serial
+    launches; the 64-byte block holds result (+0), out (+16), the three
+    regions' tickets (+32) and the two overlapped regions' release counters
+    (+44) -- see ``rtcg::finish``.  ``seq`` numbers the overlapped launches."""
 
     def __init__(self, acc_size: int, out_size: int, stream: int = 0) -> None:
         self.capacity = 0
         self.partials = 0
+        self.seq = 0
         self.acc_size, self.out_size = acc_size, out_size
         self.stream = stream
         self.result = _runtime.mem_alloc(64)
@@ -156,8 +167,19 @@ class _Scratch:
                 # device-wide synchronisation, which would block on peers'
                 # exchange kernels spinning on the same GPU)
                 _runtime.mem_free_async(self.partials, self.stream)
-            self.partials = _runtime.mem_alloc_async(cap * self.acc_size, self.stream)
+            self.partials = _runtime.mem_alloc_async(3 * cap * self.acc_size, self.stream)
             self.capacity = cap
+
+    def slot(self, overlapped: bool):
+        """(partials region, seq parameter) of the next launch: an overlapped
+        launch takes region ``seq & 1``, a serial one region 2.  The caller
+        commits ``seq`` (``self.seq += 1``) once an overlapped launch was
+        issued -- a number handed out but never launched would leave its
+        region unreleased."""
+        if not overlapped:
+            return self.partials + 2 * self.capacity * self.acc_size, _SERIAL
+        q = self.seq
+        return self.partials + (q & 1) * self.capacity * self.acc_size, q
 
 
 def _is_dtype_like(obj) -> bool:
@@ -242,7 +264,7 @@ class ReductionKernel:
             self.smem, self._tma_tile = tp["tma_smem"], tp["tile"]
         self.combine = jit.get_kernel(self.module, f"{name}_combine")
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
-        self._binder = cg.Binder(sig, extra=6)
+        self._binder = cg.Binder(sig, extra=7)
         self._waves = 1 if self.variant.waves is None else self.variant.waves
         self._scratch: dict[int, _Scratch] = {}
         self._lock = threading.Lock()
@@ -344,7 +366,7 @@ class ReductionKernel:
             params.append((p.is_vector, p.dtype, p.dtype.size, p.dtype.kind,
                            bool(acc and acc.used), bool(acc and acc.written)))
         plan = self._plans[dev] = _runtime.fastlaunch().Plan(
-            params, nd.NdArray, block, self.variant.workers or 0, gen, vec, 6)
+            params, nd.NdArray, block, self.variant.workers or 0, gen, vec, 7)
         return plan
 
     def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
@@ -379,12 +401,16 @@ class ReductionKernel:
             st = getattr(tls, "stream", 0) if stream is None else stream or 0
             s = self._scratch.get((dev, st, _get_ident())) or self.scratch(dev, st)
             plan = self._plans.get(dev) or self._plan(dev)
+            rotate = overlap_previous and not _runtime.stream_is_capturing(st)
+            partials, seq = s.slot(rotate)
             got = plan.launch(args, n, base, st or 0, s.capacity,
-                              (s.partials, s.result, s.out if out is None else out.address,
-                               s.ticket, 0, 0), 1 if overlap_previous else 0)
+                              (partials, s.result, s.out if out is None else out.address,
+                               s.ticket, 0, 0, seq), 1 if overlap_previous else 0)
             if got:          # None: the Python binder below; 0: empty span
                 if got < 0:
                     _runtime._check(-got, "launch")
+                if rotate:
+                    s.seq += 1
                 self.launches += 1
                 return s
         # the Python binder: empty spans, peer exchanges, and every call the
@@ -420,15 +446,20 @@ class ReductionKernel:
             grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
                                self._waves, smem)
         s.ensure(grid)
+        rotate = overlap_previous and not _runtime.stream_is_capturing(stream)
+        partials, seq = s.slot(rotate)
         b.set_range(vals, base, base + n)
-        vals[b.count + 2] = s.partials
+        vals[b.count + 2] = partials
         vals[b.count + 3] = s.result
         vals[b.count + 4] = out_addr
         vals[b.count + 5] = s.ticket
+        vals[b.count + 8] = seq
         if overlap_previous:
             _runtime.launch_overlapped(fn, grid, self.variant.block, ptrs, smem, stream)
         else:
             _runtime.launch(fn, grid, self.variant.block, ptrs, smem, stream)
+        if rotate:
+            s.seq += 1
         self.launches += 1
         return s
 

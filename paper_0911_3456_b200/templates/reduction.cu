@@ -26,7 +26,8 @@ __device__ __forceinline__ auto rtcg_map(const long i${map_params})
 extern "C" __global__ void __launch_bounds__(${block})
 ${name}_g(${kparams_generic}, const long start, const long end,
     ${acc_t} *rtcg_partials, ${acc_t} *rtcg_result, ${out_t} *rtcg_out,
-    unsigned int *rtcg_ticket, const rtcg::xr *rtcg_xr, const unsigned long long rtcg_epoch)
+    unsigned int *rtcg_ticket, const rtcg::xr *rtcg_xr, const unsigned long long rtcg_epoch,
+    const unsigned long long rtcg_seq)
 {
     asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
@@ -36,7 +37,7 @@ ${unpack}
         acc = rtcg_fold(acc, rtcg_map<${ptr_types_generic}>(i${call_args}));
     });
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch, rtcg_seq);
 }
 {% endif %}
 {% if tma %}
@@ -50,7 +51,8 @@ extern "C" __global__ void __launch_bounds__(${block})
 ${name}(${kparams_vector}, const long start, const long end,
     ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
     ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
-    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
+    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch,
+    const unsigned long long rtcg_seq)
 {
     asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
@@ -116,7 +118,7 @@ ${smem_loads}
         }
     }
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch, rtcg_seq);
 }
 {% endif %}
 {% if vector %}
@@ -126,7 +128,8 @@ extern "C" __global__ void __launch_bounds__(${block})
 ${name}(${kparams_vector}, const long start, const long end,
     ${acc_t} *__restrict__ rtcg_partials, ${acc_t} *__restrict__ rtcg_result,
     ${out_t} *__restrict__ rtcg_out, unsigned int *__restrict__ rtcg_ticket,
-    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch)
+    const rtcg::xr *__restrict__ rtcg_xr, const unsigned long long rtcg_epoch,
+    const unsigned long long rtcg_seq)
 {
     asm volatile("griddepcontrol.launch_dependents;");   // a successor may start streaming
 ${unpack}
@@ -184,7 +187,7 @@ ${vec_loads}
         }
     }
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
-                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch);
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch, rtcg_seq);
 }
 {% endif %}
 {% if combine %}

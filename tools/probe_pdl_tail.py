@@ -20,7 +20,7 @@ __device__ __forceinline__ unsigned long long gt() {
     unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 extern "C" __global__ void __launch_bounds__(256)
 pdl_probe(const float4 *__restrict__ x, long n4, unsigned long long *stamps, int launch,
-          unsigned *tickets, long long extra_ns, float *sink)
+          unsigned *tickets, long long extra_ns, float *sink, int wait_last)
 {
     asm volatile("griddepcontrol.launch_dependents;");
     const unsigned long long t0 = gt();
@@ -31,11 +31,12 @@ pdl_probe(const float4 *__restrict__ x, long n4, unsigned long long *stamps, int
         acc += v.x + v.y + v.z + v.w;
     }
     const unsigned long long t1 = gt();
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!wait_last) asm volatile("griddepcontrol.wait;" ::: "memory");
     const unsigned long long t2 = gt();
     __shared__ bool last;
     if (threadIdx.x == 0) last = atomicAdd(tickets + launch, 1u) == gridDim.x - 1;
     __syncthreads();
+    if (last && wait_last) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (last && threadIdx.x == 0) {
         const unsigned long long s = gt();
         while ((long long)(gt() - s) < extra_ns) { }
@@ -61,20 +62,21 @@ def main():
     occ = rt.occupancy(fn, 256, 0)
     launches = 6
     out = {}
-    for waves in (1, 2):
+    for waves, wait_last in ((1, 0), (2, 0), (1, 1), (2, 1)):
         grid = sms * occ * waves
         stamps = rt.mem_alloc(launches * grid * 4 * 8)
         tickets = rt.mem_alloc(4 * launches)
         sink = rt.mem_alloc(4)
         for extra_us in (0, 5, 20):
-            for overlap in (False, True):
+            for overlap in ((True,) if wait_last else (False, True)):
                 best, tl = float("inf"), None
                 for _ in range(3):
                     rt.memset_async(tickets, 0, 4 * launches)
                     rt.synchronize()
                     vals = [ctypes.c_uint64(x), ctypes.c_int64(n4), ctypes.c_uint64(stamps),
                             ctypes.c_int32(0), ctypes.c_uint64(tickets),
-                            ctypes.c_int64(extra_us * 1000), ctypes.c_uint64(sink)]
+                            ctypes.c_int64(extra_us * 1000), ctypes.c_uint64(sink),
+                            ctypes.c_int32(wait_last)]
                     s, e = rt.Event(), rt.Event()
                     s.record()
                     for k in range(launches):
@@ -96,7 +98,8 @@ def main():
                                     for b in range(grid)]
                             tl.append((min(r[0] for r in rows), max(r[3] for r in rows)))
                 base = tl[0][0]
-                key = f"waves{waves}_extra{extra_us}us_{'pdl' if overlap else 'serial'}"
+                key = (f"waves{waves}_{'waitlast' if wait_last else 'waitall'}_extra{extra_us}us_"
+                       f"{'pdl' if overlap else 'serial'}")
                 out[key] = {"us_per_launch": round(best * 1e3 / launches, 2),
                             "launch_start_end_us": [(round((a - base) / 1e3, 1),
                                                      round((b - base) / 1e3, 1)) for a, b in tl]}
