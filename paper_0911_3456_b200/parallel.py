@@ -35,6 +35,7 @@ import numpy as np
 
 from . import _runtime
 from . import ndarray as nd
+from .reduction import _host_slot
 
 __all__ = ["shard_range", "ShardedArray", "scatter_from_host", "sharded_elementwise",
            "sharded_reduce", "gather_partials", "ordered_fold", "nccl_op", "PeerMailbox",
@@ -392,16 +393,19 @@ def sharded_reduce(kernel, *args, group=None, return_device: bool = False,
     if collective == "p2p":
         mailbox = peer_mailbox(group, stream)
         with _runtime.use_stream(stream):
-            first = next(a for a in local_args if isinstance(a, nd.NdArray))
-            out = first.pool.alloc_uninitialized(spec.out_dtype, ())
-            kernel.launch(*local_args, n=n_local, base=base, out=out, peers=mailbox,
-                          overlap_previous=overlap_previous)
             if return_device:
+                first = next(a for a in local_args if isinstance(a, nd.NdArray))
+                out = first.pool.alloc_uninitialized(spec.out_dtype, ())
+                kernel.launch(*local_args, n=n_local, base=base, out=out, peers=mailbox,
+                              overlap_previous=overlap_previous)
                 return out
-            value = out.to_host()
-            out.free()
+            # the global value lands in this thread's page-locked slot
+            slot = _host_slot()
+            kernel.launch(*local_args, n=n_local, base=base, peers=mailbox,
+                          overlap_previous=overlap_previous, out_address=slot)
+            _runtime.stream_synchronize(stream)
             mailbox.check(stream)
-            return spec.out_dtype.np.type(value[()])
+            return spec.out_dtype.np.type(nd.ctype_for(spec.out_dtype).from_address(slot).value)
     with _runtime.use_stream(stream):
         scratch = kernel.launch(*local_args, n=n_local, base=base)
         acc_view = torch.as_tensor(_DeviceView(scratch.result, 1, spec.acc_dtype), device="cuda")

@@ -133,6 +133,20 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
 
 
 _SERIAL = 1 << 63
+_host_slots = threading.local()
+
+
+def _host_slot() -> int:
+    """This thread's 64-byte page-locked result slot.  A synchronous call
+    (``kernel(x)`` returning a host scalar) passes it as the kernel's ``out``:
+    with unified addressing the last CTA stores the value straight into host
+    memory, so the call is launch + stream synchronisation, without a
+    device-to-host copy (the call returns before the thread's next one, so
+    one slot per thread serves every kernel and device)."""
+    slot = getattr(_host_slots, "address", 0)
+    if not slot:
+        slot = _host_slots.address = _runtime.host_alloc(64)
+    return slot
 
 
 class _Scratch:
@@ -370,7 +384,8 @@ class ReductionKernel:
         return plan
 
     def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
-               out: nd.NdArray | None = None, peers=None, overlap_previous: bool = False):
+               out: nd.NdArray | None = None, peers=None, overlap_previous: bool = False,
+               out_address: int = 0):
         """Asynchronous stage 1+2.  Returns the scratch (result address holds
         the accumulator, ``out`` -- or the scratch out slot -- the out-dtype
         value).  Used by ``__call__`` and by the multi-GPU driver.
@@ -390,7 +405,10 @@ class ReductionKernel:
         the stream writes nothing this call reads (its inputs).  With
         ``peers``, one GPU per rank is assumed (ranks emulated on one GPU
         share its SMs with each other's waiting grids).  Measured on B200:
-        back-to-back dot f32 at 2^24 / 2^26 / 2^28 +19 / +5 / +2 %."""
+        back-to-back dot f32 at 2^24 / 2^26 / 2^28 +19 / +5 / +2 %.
+
+        ``out_address`` (internal) overrides the out slot with a raw address
+        -- the page-locked host slot of a synchronous call."""
         if stream is not None:
             stream = getattr(stream, "handle", stream)
         if peers is None:
@@ -403,8 +421,9 @@ class ReductionKernel:
             plan = self._plans.get(dev) or self._plan(dev)
             rotate = overlap_previous and not _runtime.stream_is_capturing(st)
             partials, seq = s.slot(rotate)
+            oaddr = out.address if out is not None else out_address or s.out
             got = plan.launch(args, n, base, st or 0, s.capacity,
-                              (partials, s.result, s.out if out is None else out.address,
+                              (partials, s.result, oaddr,
                                s.ticket, 0, 0, seq), 1 if overlap_previous else 0)
             if got:          # None: the Python binder below; 0: empty span
                 if got < 0:
@@ -420,7 +439,7 @@ class ReductionKernel:
         vals, ptrs, vectors, n = self._binder.bind(args, n, base, self.name, _ERRORS)
         dev = _runtime.current_device()
         s = self.scratch(dev, stream)
-        out_addr = out.address if out is not None else s.out
+        out_addr = out.address if out is not None else out_address or s.out
         b = self._binder
         if peers is not None:
             # resolve (and load) every entry point before the first exchange
@@ -570,8 +589,11 @@ class ReductionKernel:
             out = first.pool.alloc_uninitialized(self.spec.out_dtype, ())
             self.launch(*args, n=n, base=base, stream=stream, out=out)
             return out
-        s = self.launch(*args, n=n, base=base, stream=stream)
-        return self._read(s.out, self.spec.out_dtype, stream)
+        slot = _host_slot()
+        self.launch(*args, n=n, base=base, stream=stream, out_address=slot)
+        _runtime.stream_synchronize(None if stream is None else getattr(stream, "handle", stream))
+        dt = self.spec.out_dtype
+        return dt.np.type(nd.ctype_for(dt).from_address(slot).value)
 
 
 def make_reduction(signature, out_dtype, neutral: str, reduce_expr: str,

@@ -259,6 +259,33 @@ def test_threads_sharing_a_kernel_get_their_own_results(kernel_env):
         assert all(ex.map(worker, range(8)))
 
 
+def test_synchronous_results_land_in_the_host_slot(kernel_env):
+    """``kernel(x)`` has the last CTA store the value straight into a
+    page-locked host slot (one per thread, shared by every kernel): calls
+    alternating kernels, dtypes, empty spans (the combine kernel writes the
+    neutral), streams and device-returning calls each read their own value."""
+    from paper_0911_3456_b200 import _runtime
+    kwargs, pool = kernel_env
+    i8 = nd.from_host(pool, nd.int8, [-7, 3, 100, -128])
+    f64 = nd.from_host(pool, nd.float64, np.arange(1000, dtype=np.float64))
+    u64 = nd.from_host(pool, nd.uint64, np.full(5000, 3, np.uint64))
+    mx8, s64, su = (rd.max_kernel(nd.int8, **kwargs), rd.sum_kernel(nd.float64, **kwargs),
+                    rd.sum_kernel(nd.uint64, **kwargs))
+    st = _runtime.Stream()
+    for rep in range(20):
+        assert mx8(i8) == 100
+        assert s64(f64) == 499500.0
+        assert s64(f64, n=0) == 0.0
+        assert su(u64, stream=st) == 15000
+        assert mx8(i8, n=2) == 3
+        dev = s64(f64, return_device=True)
+        assert s64(f64, n=10) == 45.0
+        assert dev.to_host()[()] == 499500.0
+        dev.free()
+    assert rd._host_slot() == rd._host_slot()
+    st.close()
+
+
 @pytest.mark.parametrize("unroll,block,workers", [(1, 256, 296), (2, 128, 592), (4, 64, 148)])
 def test_prefetch_pipeline_is_bit_identical(kernel_env, unroll, block, workers):
     """prefetch=True only moves loads earlier: with the same grid (pinned
