@@ -528,7 +528,6 @@ class ReductionKernel:
                                        f"kernel span is {total}")
         dev = _runtime.current_device()
         pool = nd.default_pool(dev)
-        out = pool.alloc_uninitialized(self.spec.out_dtype, ())
         step = chunk or max(1 << 16, self.HOST_CHUNK_BYTES // max(1, host_bytes) // 256 * 256)
         step = max(1, min(step, total)) if total > 0 else 1
         count = -(-total // step) if total > 0 else 0
@@ -562,12 +561,15 @@ class ReductionKernel:
             done = True
             s = self.scratch(dev)
             s.ensure(1)
-            self._launch_combine(accs.address, count, s.result, out.address)
             if want_device:
+                out = pool.alloc_uninitialized(self.spec.out_dtype, ())
+                self._launch_combine(accs.address, count, s.result, out.address)
                 return out
-            value = self._read(out.address, self.spec.out_dtype)
-            out.free()
-            return value
+            slot = _host_slot()
+            self._launch_combine(accs.address, count, s.result, slot)
+            _runtime.stream_synchronize()
+            dt = self.spec.out_dtype
+            return dt.np.type(nd.ctype_for(dt).from_address(slot).value)
         finally:
             if not done:       # drain in-flight copies before the staging is reused
                 for st in streams:
