@@ -215,7 +215,7 @@ def test_dropped_arrays_return_to_the_pool():
     assert s["bytes_held"] == held_before + 4096 and s["bytes_outstanding"] == 0
     b = pool.alloc(nd.float32, (1000,))
     assert pool.stats()["pool_hits"] == 1
-    pool.free(b)           # explicit free detaches the finalizer: no double return
+    pool.free(b)           # an explicit free leaves nothing for the GC: no double return
     del b
     gc.collect()
     assert pool.stats()["bytes_held"] == 4096
