@@ -136,17 +136,32 @@ _SERIAL = 1 << 63
 _host_slots = threading.local()
 
 
+class _HostSlot:
+    """A 64-byte page-locked buffer, returned to the driver when its thread's
+    local storage goes away."""
+    __slots__ = ("address",)
+
+    def __init__(self) -> None:
+        self.address = _runtime.host_alloc(64)
+
+    def __del__(self):
+        try:
+            _runtime.host_free(self.address)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
 def _host_slot() -> int:
-    """This thread's 64-byte page-locked result slot.  A synchronous call
+    """This thread's page-locked result slot.  A synchronous call
     (``kernel(x)`` returning a host scalar) passes it as the kernel's ``out``:
     with unified addressing the last CTA stores the value straight into host
     memory, so the call is launch + stream synchronisation, without a
     device-to-host copy (the call returns before the thread's next one, so
     one slot per thread serves every kernel and device)."""
-    slot = getattr(_host_slots, "address", 0)
-    if not slot:
-        slot = _host_slots.address = _runtime.host_alloc(64)
-    return slot
+    slot = getattr(_host_slots, "slot", None)
+    if slot is None:
+        slot = _host_slots.slot = _HostSlot()
+    return slot.address
 
 
 class _Scratch:
