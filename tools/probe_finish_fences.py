@@ -11,7 +11,10 @@ serial launches replayed (device time per launch, no host path), and 20
 back-to-back overlapped launches (the bench's protocol).  Five alternating
 rounds, best of each.
 
-    python tools/probe_finish_fences.py > gpurun_out/finish_fences.json
+    python tools/probe_finish_fences.py [fences|division] > gpurun_out/finish_fences.json
+
+(``division``: the last CTA's partial ranges with 32-bit instead of 64-bit
+division, the same values.)
 """
 import json
 import sys
@@ -23,6 +26,21 @@ import numpy as np  # noqa: E402
 from paper_0911_3456_b200 import _codegen as cg, _runtime as rt, graph  # noqa: E402
 from paper_0911_3456_b200 import ndarray as nd, reduction as rd  # noqa: E402
 
+DIV_NEW = """    // thread t folds partials [t*g/b, (t+1)*g/b); 32-bit division whenever
+    // (t+1)*g fits (g < 2^22 -- every practical grid), 64-bit otherwise
+    const unsigned g = gridDim.x, b = blockDim.x, t = threadIdx.x;
+    unsigned long lo, hi;
+    if (g < (1u << 22)) {
+        lo = t * g / b;
+        hi = (t + 1) * g / b;
+    } else {
+        lo = (unsigned long)t * g / b;
+        hi = (unsigned long)(t + 1) * g / b;
+    }
+"""
+DIV_OLD = """    const unsigned long g = gridDim.x, b = blockDim.x, t = threadIdx.x;
+    const unsigned long lo = t * g / b, hi = (t + 1) * g / b;
+"""
 NEW = """        last_cta = atom_add_acq_rel_gpu_u32(ticket + slot, 1u) == gridDim.x - 1;
     }
     __syncthreads();        // thread 0's acquire orders the whole CTA's loads
@@ -39,18 +57,22 @@ OLD = """        __threadfence();
 """
 
 
+WHAT = sys.argv[1] if len(sys.argv) > 1 else "fences"
+
+
 def build(old: bool):
     real = cg.template
 
     def patched(name):
         text = real(name)
         if name == "prelude.cuh" and old:
-            assert NEW in text
-            text = text.replace(NEW, OLD)
+            a, b = (DIV_NEW, DIV_OLD) if WHAT == "division" else (NEW, OLD)
+            assert a in text
+            text = text.replace(a, b)
         return text
     cg.template = patched
     try:
-        tag = "old" if old else "new"
+        tag = ("old" if old else "new") + WHAT[:3]
         return {"sum": rd.ReductionKernel(rd.ReductionSpec("float *x", nd.float32, "0", "a + b",
                                                            None), f"sum_{tag}"),
                 "max": rd.ReductionKernel(rd.ReductionSpec("float *x", nd.float32, "-INFINITY",
