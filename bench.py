@@ -590,20 +590,22 @@ class Ctx:
         self.d.barrier()
         return self.d.bcast(best)
 
-    def reducer(self, kernel):
+    def reducer(self, kernel, overlap: bool = True):
         """Step function of a global reduction of sharded args over the
         ranks (in-kernel peer exchange, NCCL, or gloo); returns
-        (step(*sharded) -> 0-d out array, launches per step)."""
+        (step(*sharded) -> 0-d out array, launches per step).  ``overlap``:
+        programmatic dependent launches (back-to-back steps); off for calls
+        timed one at a time, where a plain launch is what a caller gets."""
         d, par = self.d, self.par
         if not d.distributed:
             def step(*args, out):
-                kernel.launch(*[a.local for a in args], out=out, overlap_previous=True)
+                kernel.launch(*[a.local for a in args], out=out, overlap_previous=overlap)
             return step, 1
         coll = self.collective
 
         def step(*args, out=None):
             par.sharded_reduce(kernel, *args, return_device=True, collective=coll,
-                               overlap_previous=coll == "p2p").free()
+                               overlap_previous=overlap and coll == "p2p").free()
         return step, 1 if coll == "p2p" else 2
 
     def global_value(self, kernel, *args):
@@ -1159,7 +1161,7 @@ def c5_sweep(c: Ctx) -> dict:
                 gb(3 * dt.size * m, ms)
             for name, k in kernels.items():
                 args = (sx, sy) if name == "dot" else (sx,)
-                step, _ = c.reducer(k)
+                step, _ = c.reducer(k, overlap=False)     # timed one call at a time
                 o = c.pool.alloc_uninitialized(k.spec.out_dtype, ())
                 ms = dev_ms(lambda: step(*args, out=o))
                 nb = (2 if name == "dot" else 1) * dt.size * m
