@@ -281,3 +281,22 @@ def test_host_argument_handlers_and_views():
     g.free()
     with pytest.raises(ValueError):
         g[0:1]
+
+
+@pytest.mark.timeout(60)
+def test_collection_inside_the_pool_lock_does_not_deadlock():
+    """A cyclic garbage collection can run while the pool holds its lock (any
+    allocation inside the locked section); an unreachable array in a cycle
+    then returns its block from __del__ on the same thread."""
+    import gc
+    dev = HostDevice()
+    pool = dev.pool()
+
+    class Holder:
+        pass
+    h = Holder()
+    h.me, h.arr = h, pool.alloc(nd.float32, (100,))
+    del h                                   # now only reachable through its own cycle
+    with pool._lock:
+        gc.collect()                        # __del__ -> _give_back on this thread
+    assert pool.stats()["bytes_outstanding"] == 0
