@@ -502,6 +502,40 @@ def test_double_sin_cos_within_two_ulp_of_glibc(kernel_env):
     assert np.all(np.isnan(out.to_host()))
 
 
+@pytest.mark.parametrize("fn", ["sin", "cos"])
+def test_double_sin_cos_bit_identical_to_cuda_library(kernel_env, fn):
+    """The prelude's lean sin / cos (templates/prelude.cuh ``rtcg_trig``)
+    return exactly the bits of CUDA's own double sin / cos (torch calls the
+    library) -- on |x| < 2^31 by construction, beyond it, at inf / NaN and
+    the signed zeros by the out-of-line library call -- over several
+    magnitudes, next to multiples of pi/2, both quadrant parities, and
+    through the vector, prefetch and cp.async-ring entry points."""
+    torch = pytest.importorskip("torch")
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(41)
+    half_pi = np.pi / 2
+    k = np.arange(-5000, 5000, dtype=np.float64)
+    near = np.concatenate([k * half_pi, np.nextafter(k * half_pi, -np.inf),
+                           np.nextafter(k * half_pi, np.inf), (k + 0.5) * half_pi])
+    x = np.concatenate([rng.uniform(-2, 2, 200_000), rng.uniform(-1e3, 1e3, 100_000),
+                        rng.uniform(-2.0**31, 2.0**31, 100_000), near,
+                        np.ldexp(rng.uniform(-1, 1, 20_000), rng.integers(-1074, 31, 20_000)),
+                        rng.uniform(2.0**31 - 64, 2.0**31 + 64, 1000),
+                        [2.0**31, -2.0**31, np.nextafter(2.0**31, 0), 1e300, -1e22,
+                         0.0, -0.0, 5e-324, -5e-324, np.inf, -np.inf, np.nan]])
+    want = getattr(torch, fn)(torch.from_numpy(x).cuda()).cpu().numpy()
+    gx = nd.from_host(pool, nd.float64, x)
+    for v in (ew.VariantParams(), ew.VariantParams(block=128, waves=4, prefetch=True),
+              ew.VariantParams(block=256, unroll=2, waves=2, stages=2)):
+        kern = ew.ElementwiseKernel("double *x, double *z", f"z[i] = {fn}(x[i])", f"b_{fn}",
+                                    v, **kwargs)
+        gz = pool.alloc(nd.float64, x.shape)
+        kern(gx, gz)
+        got = gz.to_host()
+        same = (got.view(np.int64) == want.view(np.int64)) | (np.isnan(got) & np.isnan(want))
+        assert same.all(), (fn, v, x[~same][:5], got[~same][:5], want[~same][:5])
+
+
 
 @pytest.mark.parametrize("stages, unroll, block", [(2, 1, 128), (3, 2, 256), (4, 1, 256),
                                                    (8, 4, 64), (6, 1, 1024)])
