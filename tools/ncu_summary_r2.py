@@ -28,6 +28,9 @@ KERNELS = {
     "polysin": ("polysin_ring", {"block": 512, "unroll": 2, "waves": 2, "stages": 2}, 16 * N),
     "polysin_prefetch": ("polysin_pref", {"block": 256, "unroll": 1, "waves": 1,
                                           "prefetch": True}, 16 * N),
+    # the prelude's lean double sin (templates/prelude.cuh rtcg_trig)
+    "polysin_leansin": ("polysin_leansin", {"block": 128, "unroll": 1, "waves": 4,
+                                            "prefetch": True}, 16 * N),
     "maxabs": ("maxabs", {"block": 1024, "unroll": 1, "waves": 2}, 4 * N),
     "sumsq": ("sumsq", {"block": 256, "unroll": 1, "waves": 2}, 4 * N),
     "sum_i64": ("sum_i64", {"block": 256, "unroll": 8, "waves": 2}, 8 * N),
