@@ -484,6 +484,46 @@ def stock_cpu(kind: str, arrays: list, nbytes: int, warmup: int = 1, calls: int 
                       f"best of {max(1, calls)} after {max(1, warmup)} warm-up"}
 
 
+def stock_c5(dname: str, hx: np.ndarray, hy: np.ndarray, reps: int = 5) -> dict:
+    """One C5 row on the unmodified reference (``baseline/_ref``, default
+    variant, all host cores): the same ops on the same values as the GPU
+    row -- ``x + y`` and the eager chain through the reference's NdArray
+    operators, its stock sum / max / dot kernels; wall time per call
+    (best of ``reps`` after a warm-up), microseconds."""
+    stock = _stock_reference()
+    if stock is None:
+        return {"error": "baseline/_ref not installed"}
+    rnd, rrd = stock
+    pool = rnd.MemoryPool()
+    dt = rnd.BY_NAME[dname]
+    gx, gy = rnd.from_host(pool, dt, hx), rnd.from_host(pool, dt, hy)
+    sk, mk, dk = rrd.sum_kernel(dt), rrd.max_kernel(dt), rrd.dot_kernel(dt)
+
+    def add():
+        gx.__add__(gy).free()
+
+    def chain():
+        t1 = gx * 2
+        t2 = t1 + gy
+        t3 = t2 - gx
+        for t in (t1, t2, t3):
+            t.free()
+    ops = {"add": add, "chain_eager": chain, "sum": lambda: sk(gx), "max": lambda: mk(gx),
+           "dot": lambda: dk(gx, gy)}
+    out = {}
+    for name, fn in ops.items():
+        fn()
+        best = math.inf
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        out[f"{name}_us"] = round(best * 1e6, 2)
+    gx.free()
+    gy.free()
+    return out
+
+
 def run_reference(args) -> int:
     """CPU reference arm: rank 0 only, no GPU or process group needed."""
     if _env_int("RANK", 0) != 0:
@@ -1058,7 +1098,12 @@ def c5_sweep(c: Ctx) -> dict:
     {x+y, eager chain (x*2 + y) - x, fused chain, sum, max, dot}; device
     time per call (best of 5 after a warm-up, max over ranks); sizes whose
     three arrays fit in L2 are flagged.  Plus compile latency (cold NVRTC vs
-    warm cache construction) and an autotune campaign vs its store hit."""
+    warm cache construction) and an autotune campaign vs its store hit.
+    At N = 1, sizes up to 2^24 also run on the unmodified reference's CPU
+    path (``ref_cpu``) and through this package's public calls as a caller
+    sees them (``wall``: synchronised wall time); ``*_speedup_vs_ref`` is
+    wall over wall.  Float rows check sum (n*eps rule) and max (exact),
+    integer rows wrapping sum and max exactly."""
     d, rt, at, ew, nd, par, rd = c.d, c.rt, c.at, c.ew, c.nd, c.par, c.rd
     from paper_0911_3456_b200 import fusion, jit
     res = {"latency": {}, "autotune": {}, "rows": {}}
@@ -1167,6 +1212,50 @@ def c5_sweep(c: Ctx) -> dict:
                 nb = (2 if name == "dot" else 1) * dt.size * m
                 row[f"{name}_us"], row[f"{name}_GBs"] = round(ms * 1e3, 2), gb(nb, ms)
                 o.free()
+            # the reference's CPU path on the same values (rank 0 at N = 1,
+            # sizes whose reference calls take milliseconds)
+            if d.world == 1 and lg <= 24 and not c.args.no_cpu:
+                try:
+                    ref = stock_c5(dname, x.to_host(), y.to_host())
+                    row["ref_cpu"] = ref
+                    # this side as the caller sees it: wall time of the
+                    # public call, synchronised (host scalars for reductions)
+                    mine = {"add": lambda: (add(x, y, z), rt.synchronize()),
+                            "chain_eager": lambda: (eager(), rt.synchronize()),
+                            "sum": lambda: kernels["sum"](x), "max": lambda: kernels["max"](x),
+                            "dot": lambda: kernels["dot"](x, y)}
+                    wall = {}
+                    for op_name, fn in mine.items():
+                        fn()
+                        best = math.inf
+                        for _ in range(5):
+                            t0 = time.perf_counter()
+                            fn()
+                            best = min(best, time.perf_counter() - t0)
+                        wall[f"{op_name}_us"] = round(best * 1e6, 2)
+                    row["wall"] = wall
+                    for op_name in mine:
+                        if f"{op_name}_us" in ref:
+                            row[f"{op_name}_speedup_vs_ref"] = round(
+                                ref[f"{op_name}_us"] / wall[f"{op_name}_us"], 1)
+                except Exception as exc:  # noqa: BLE001 - report, don't fail the bench
+                    row["ref_cpu"] = {"error": str(exc)[:200]}
+            # float rows: sum within the n*eps rule of the fp64 oracle (the
+            # reference's float32 sums accumulate in double), max exact
+            if dt.kind == "f":
+                t = c.torch.as_tensor(x, device="cuda").double()
+                want_s = sum(d.gather(float(t.sum().item())))
+                mag = sum(d.gather(float(t.abs().sum().item())))
+                want_m = max(d.gather(float(t.max().item())))
+                got_s = float(c.global_value(kernels["sum"], sx))
+                got_m = float(c.global_value(kernels["max"], sx))
+                ulp = float(np.spacing(np.float32(abs(want_s)))) if dname == "float32" else \
+                    float(np.spacing(abs(want_s)))
+                tol = 0.5 * ulp + total * 2.0 ** -53 * mag
+                row["parity_ok"] = abs(got_s - want_s) <= tol and got_m == want_m
+                ok_all &= row["parity_ok"]
+                del t
+                c.torch.cuda.empty_cache()
             # integer rows: exact checks of the global results vs torch
             if dt.kind == "i":
                 t = c.torch.as_tensor(x, device="cuda")
