@@ -131,5 +131,19 @@ with g.capture():
 g.launch()
 g.synchronize()
 assert int(o.get()) == (1 << 20) * ((1 << 20) - 1) // 2
+# the prelude's sin / cos (coefficient-table loads, the out-of-line library
+# call for |x| >= 2^31, inf and NaN) through vector, prefetch and ring entries
+# and a reduction map
+trig_x = np.concatenate([rng.uniform(-4, 4, 5001), [0.0, -0.0, 2.0**31, -1e300, np.inf, np.nan]])
+tx = nd.from_host(pool, nd.float64, trig_x)
+tz = pool.alloc(nd.float64, trig_x.shape)
+for v in (ew.VariantParams(), ew.VariantParams(block=128, waves=4, prefetch=True),
+          ew.VariantParams(block=256, unroll=2, waves=2, stages=2)):
+    ew.ElementwiseKernel("double *x, double *z", "z[i] = sin(x[i]) + cos(x[i])", "trig", v)(tx, tz)
+    checks += 1
+want = np.sin(trig_x[:5001]) + np.cos(trig_x[:5001])
+assert np.allclose(tz.get()[:5001], want, rtol=0, atol=1e-14)
+rd.make_reduction("double *x", nd.float64, "0", "a + b", "sin(x[i])", "sum_sin")(tx[:5001])
+checks += 1
 rt.synchronize()
 print(f"sanitize paths ok ({checks} launches checked)")
