@@ -163,3 +163,20 @@ def test_reduction_check_bound_and_bit_equality():
     assert chk["ok"] and chk["bit_equal_f32_fsum"] and chk["ulps"] < 1e-6
     far = bench.reduction_check(got + 1e-3, exact, n=4, sum_abs=1.0)
     assert not far["ok"] and not far["bit_equal_f32_fsum"]
+
+
+def test_stock_c5_times_the_reference_ops():
+    """The C5 CPU leg runs the unmodified reference's operators and stock
+    reductions (skipped where baseline/_ref is not installed)."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT))
+    import bench
+    if bench._stock_reference() is None:
+        pytest.skip("baseline/_ref not installed")
+    rng = np.random.default_rng(9)
+    for dname, dt in (("float32", np.float32), ("int64", np.int64)):
+        x = (rng.integers(-1000, 1000, 4096) / (1000 if dt is np.float32 else 1)).astype(dt)
+        y = (rng.integers(-1000, 1000, 4096) / (1000 if dt is np.float32 else 1)).astype(dt)
+        got = bench.stock_c5(dname, x, y, reps=2)
+        assert set(got) == {"add_us", "chain_eager_us", "sum_us", "max_us", "dot_us"}
+        assert all(v > 0 for v in got.values())
