@@ -1443,6 +1443,15 @@ def run_ours(args) -> int:
             config[f"c4_{name}_gbs"] = workloads[name]["GB/s"]
     if "dot_strong_2p28_total" in workloads:
         config["strong_dot_gbs"] = workloads["dot_strong_2p28_total"]["GB/s"]
+    # the elementwise configs as scalars too (parsers keep flat keys)
+    if "GB/s" in workloads.get("axpy_f32_2p28", {}):
+        config["c1_axpy_f32_2p28_gbs"] = workloads["axpy_f32_2p28"]["GB/s"]
+    ps = workloads.get("polysin_f64_2p28", {})
+    if "GB/s" in ps:
+        config["c3_polysin_f64_2p28_gbs"] = ps["GB/s"]
+        config["c3_polysin_f64_2p28_frac"] = ps["frac"]
+        config["c3_polysin_fma_gbs"] = (ps.get("fma") or {}).get("GB/s")
+        config["c3_polysin_e2e_gbs"] = (ps.get("e2e") or {}).get("value")
     line = {
         "metric": METRIC, "value": round(h["value_gbs"], 2), "unit": "GB/s", "n_gpus": d.world,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(h["step_ms"], 4),
