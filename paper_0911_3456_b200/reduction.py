@@ -31,6 +31,7 @@ from __future__ import annotations
 import ctypes
 import re
 import threading
+from time import perf_counter as _perf_counter
 from dataclasses import dataclass
 from threading import get_ident as _get_ident
 
@@ -133,16 +134,20 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
 
 
 _SERIAL = 1 << 63
+_HOST_FLAG = 1 << 62       # seq bit: out is a host slot, write its completion word
+_SPIN_S = 200e-6           # a synchronous call spins this long before blocking
 _host_slots = threading.local()
 
 
 class _HostSlot:
     """A 64-byte page-locked buffer, returned to the driver when its thread's
-    local storage goes away."""
-    __slots__ = ("address",)
+    local storage goes away: the value at +0, the completion word the last
+    CTA stores after it at +32."""
+    __slots__ = ("address", "done")
 
     def __init__(self) -> None:
         self.address = _runtime.host_alloc(64)
+        self.done = ctypes.c_uint32.from_address(self.address + 32)
 
     def __del__(self):
         try:
@@ -151,17 +156,40 @@ class _HostSlot:
             pass
 
 
+def _slot_object() -> _HostSlot:
+    slot = getattr(_host_slots, "slot", None)
+    if slot is None:
+        slot = _host_slots.slot = _HostSlot()
+    return slot
+
+
 def _host_slot() -> int:
     """This thread's page-locked result slot.  A synchronous call
     (``kernel(x)`` returning a host scalar) passes it as the kernel's ``out``:
     with unified addressing the last CTA stores the value straight into host
-    memory, so the call is launch + stream synchronisation, without a
-    device-to-host copy (the call returns before the thread's next one, so
-    one slot per thread serves every kernel and device)."""
-    slot = getattr(_host_slots, "slot", None)
-    if slot is None:
-        slot = _host_slots.slot = _HostSlot()
-    return slot.address
+    memory, so the call is launch + wait, without a device-to-host copy (the
+    call returns before the thread's next one, so one slot per thread serves
+    every kernel and device)."""
+    return _slot_object().address
+
+
+def _await_slot(slot: _HostSlot, stream) -> None:
+    """Wait for a launch that writes ``slot``'s completion word: spin on the
+    word (the last CTA stores it after the value, system-scope release) for
+    up to ``_SPIN_S``, then block on the stream -- which also reports a
+    failed launch.  Spinning saves the stream synchronisation's wake-up
+    (2^16 sum: 14.3 -> 10.8 us per call, tools/probe_sync_spin.py)."""
+    done = slot.done
+    if done.value:
+        return
+    deadline = _perf_counter() + _SPIN_S
+    while True:
+        for _ in range(64):
+            if done.value:
+                return
+        if _perf_counter() > deadline:
+            _runtime.stream_synchronize(stream)
+            return
 
 
 class _Scratch:
@@ -178,6 +206,7 @@ class _Scratch:
         self.capacity = 0
         self.partials = 0
         self.seq = 0
+        self.host_flagged = False    # the last launch stores a host slot's completion word
         self.acc_size, self.out_size = acc_size, out_size
         self.stream = stream
         self.result = _runtime.mem_alloc(64)
@@ -400,7 +429,7 @@ class ReductionKernel:
 
     def launch(self, *args, n: int | None = None, base: int = 0, stream=None,
                out: nd.NdArray | None = None, peers=None, overlap_previous: bool = False,
-               out_address: int = 0):
+               out_address: int = 0, host_flag: bool = False):
         """Asynchronous stage 1+2.  Returns the scratch (result address holds
         the accumulator, ``out`` -- or the scratch out slot -- the out-dtype
         value).  Used by ``__call__`` and by the multi-GPU driver.
@@ -423,9 +452,14 @@ class ReductionKernel:
         back-to-back dot f32 at 2^24 / 2^26 / 2^28 +19 / +5 / +2 %.
 
         ``out_address`` (internal) overrides the out slot with a raw address
-        -- the page-locked host slot of a synchronous call."""
+        -- the page-locked host slot of a synchronous call; ``host_flag``
+        (internal) makes the kernel store the slot's completion word after
+        the value.  ``scratch.host_flagged`` tells whether this launch will
+        (an empty span folds through the combine entry, which does not)."""
         if stream is not None:
             stream = getattr(stream, "handle", stream)
+        # the completion word lives in a host slot only (out + 32)
+        host_flag = bool(host_flag and out_address and out is None)
         if peers is None:
             tls = _runtime._tls
             dev = getattr(tls, "device", None)
@@ -436,6 +470,8 @@ class ReductionKernel:
             plan = self._plans.get(dev) or self._plan(dev)
             rotate = overlap_previous and not _runtime.stream_is_capturing(st)
             partials, seq = s.slot(rotate)
+            if host_flag:
+                seq |= _HOST_FLAG
             oaddr = out.address if out is not None else out_address or s.out
             got = plan.launch(args, n, base, st or 0, s.capacity,
                               (partials, s.result, oaddr,
@@ -446,6 +482,7 @@ class ReductionKernel:
                 if rotate:
                     s.seq += 1
                 self.launches += 1
+                s.host_flagged = host_flag
                 return s
         # the Python binder: empty spans, peer exchanges, and every call the
         # native plan declined (it raises the reference's exceptions)
@@ -468,6 +505,7 @@ class ReductionKernel:
         if n == 0 and peers is None:
             s.ensure(1)
             self._launch_combine(s.partials, 0, s.result, out_addr, stream)
+            s.host_flagged = False
             return s
         if n == 0:
             handle, grid, smem = self.generic, 1, 0
@@ -482,6 +520,8 @@ class ReductionKernel:
         s.ensure(grid)
         rotate = overlap_previous and not _runtime.stream_is_capturing(stream)
         partials, seq = s.slot(rotate)
+        if host_flag:
+            seq |= _HOST_FLAG
         b.set_range(vals, base, base + n)
         vals[b.count + 2] = partials
         vals[b.count + 3] = s.result
@@ -495,6 +535,7 @@ class ReductionKernel:
         if rotate:
             s.seq += 1
         self.launches += 1
+        s.host_flagged = host_flag
         return s
 
     def launch_config(self, *args, n: int | None = None) -> dict:
@@ -606,11 +647,17 @@ class ReductionKernel:
             out = first.pool.alloc_uninitialized(self.spec.out_dtype, ())
             self.launch(*args, n=n, base=base, stream=stream, out=out)
             return out
-        slot = _host_slot()
-        self.launch(*args, n=n, base=base, stream=stream, out_address=slot)
-        _runtime.stream_synchronize(None if stream is None else getattr(stream, "handle", stream))
+        slot = _slot_object()
+        st = None if stream is None else getattr(stream, "handle", stream)
+        slot.done.value = 0
+        s = self.launch(*args, n=n, base=base, stream=stream, out_address=slot.address,
+                        host_flag=True)
+        if s.host_flagged:
+            _await_slot(slot, st)
+        else:
+            _runtime.stream_synchronize(st)
         dt = self.spec.out_dtype
-        return dt.np.type(nd.ctype_for(dt).from_address(slot).value)
+        return dt.np.type(nd.ctype_for(dt).from_address(slot.address).value)
 
 
 def make_reduction(signature, out_dtype, neutral: str, reduce_expr: str,

@@ -286,6 +286,34 @@ def test_synchronous_results_land_in_the_host_slot(kernel_env):
     st.close()
 
 
+def test_synchronous_call_waits_on_the_completion_word(kernel_env):
+    """A synchronous call spins on its host slot's completion word (stored
+    by the last CTA after the value) and blocks on the stream only after
+    ``_SPIN_S``: behind a long kernel queued on the same stream the value is
+    still this call's, and the word is set exactly when the kernel wrote
+    the slot (empty spans fold through the combine entry and block)."""
+    kwargs, pool = kernel_env
+    big = pool.alloc(nd.float64, (1 << 27,))
+    fill = ew.ElementwiseKernel("double *z", "z[i] = sin((double) i)", "fill_big", **kwargs)
+    x = nd.from_host(pool, nd.float32, np.arange(1, 4097, dtype=np.float32))
+    s = rd.sum_kernel(nd.float32, **kwargs)
+    slot = rd._slot_object()
+    for rep in range(5):
+        fill(big)                           # ~1 ms of queued work ahead of the sum
+        assert s(x) == 4096 * 4097 / 2
+        assert slot.done.value == 1
+        assert s(x, n=100) == 5050.0        # no queued work: the spin path
+        assert s(x, n=0) == 0.0             # combine entry: no completion word
+        assert slot.done.value == 0
+    # a device-returning call and launch() without a host slot never write it
+    dev = s(x, return_device=True)
+    assert dev.to_host()[()] == 4096 * 4097 / 2 and slot.done.value == 0
+    sc = s.launch(x, host_flag=True)
+    assert sc.host_flagged is False
+    dev.free()
+    big.free()
+
+
 @pytest.mark.parametrize("unroll,block,workers", [(1, 256, 296), (2, 128, 592), (4, 64, 148)])
 def test_prefetch_pipeline_is_bit_identical(kernel_env, unroll, block, workers):
     """prefetch=True only moves loads earlier: with the same grid (pinned
