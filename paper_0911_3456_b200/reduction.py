@@ -178,7 +178,8 @@ def _await_slot(slot: _HostSlot, stream) -> None:
     word (the last CTA stores it after the value, system-scope release) for
     up to ``_SPIN_S``, then block on the stream -- which also reports a
     failed launch.  Spinning saves the stream synchronisation's wake-up
-    (2^16 sum: 14.3 -> 10.8 us per call, tools/probe_sync_spin.py)."""
+    (2^16 synchronous sum / max / dot: 14.4-15.0 -> 12.6-13.4 us per call,
+    tools/probe_sync_spin.py, profiles/r02_probe_small_n_spin.json)."""
     done = slot.done
     if done.value:
         return
