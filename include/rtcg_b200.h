@@ -158,6 +158,10 @@ int rtcg_host_alloc(uint64_t nbytes, void **ptr);
 int rtcg_host_free(void *ptr);
 int rtcg_host_register(void *ptr, uint64_t nbytes);
 int rtcg_host_unregister(void *ptr);
+/* *pinned = 1 when `ptr` lies in page-locked host memory (allocated or
+ * registered), else 0: the test rtcg_copy_htod / rtcg_copy_dtoh use to take
+ * the direct DMA path. */
+int rtcg_host_is_pinned(const void *ptr, int *pinned);
 
 /* --- streams / events ---------------------------------------------------- */
 int rtcg_stream_create(rtcg_stream_t *stream);

@@ -142,6 +142,7 @@ _PROTOTYPES = {
     "rtcg_host_alloc": (_u64, ctypes.POINTER(_vp)),
     "rtcg_host_free": (_vp,),
     "rtcg_host_register": (_vp, _u64),
+    "rtcg_host_is_pinned": (_vp, ctypes.POINTER(ctypes.c_int)),
     "rtcg_host_unregister": (_vp,),
     "rtcg_stream_create": (ctypes.POINTER(_vp),),
     "rtcg_stream_destroy": (_vp,),
@@ -664,3 +665,12 @@ def host_alloc(nbytes: int) -> int:
 
 def host_free(ptr: int) -> None:
     _check(lib().rtcg_host_free(ptr), "cuMemFreeHost")
+
+
+def host_is_pinned(ptr: int) -> bool:
+    """Whether host address ``ptr`` lies in page-locked memory (the test the
+    host copies use to DMA directly instead of staging)."""
+    current_device()
+    out = ctypes.c_int(0)
+    _check(lib().rtcg_host_is_pinned(ptr, ctypes.byref(out)), "host is pinned")
+    return bool(out.value)

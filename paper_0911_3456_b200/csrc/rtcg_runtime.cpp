@@ -96,7 +96,8 @@ struct Driver {
     X(cuMemFreeHost, CUresult(void *))                                     \
     X(cuMemHostRegister_v2, CUresult(void *, size_t, unsigned))            \
     X(cuMemHostUnregister, CUresult(void *))                               \
-    X(cuMemHostGetFlags, CUresult(unsigned *, void *))                     \
+    X(cuPointerGetAttributes,                                                  \
+      CUresult(unsigned, CUpointer_attribute *, void **, CUdeviceptr))     \
     X(cuStreamCreate, CUresult(CUstream *, unsigned))                      \
     X(cuStreamDestroy_v2, CUresult(CUstream))                              \
     X(cuStreamSynchronize, CUresult(CUstream))                             \
@@ -676,9 +677,17 @@ void stream_copy(void *dst, const void *src, size_t n) {
 #endif
 }
 
+// Page-locked (cuMemHostAlloc'd or registered) host memory reports
+// CU_MEMORYTYPE_HOST; ordinary pageable memory is not a CUDA pointer, for
+// which cuPointerGetAttributes (unlike cuMemHostGetFlags) returns success
+// with a zero type instead of an API error.
 bool is_pinned(const void *p) {
-    unsigned flags = 0;
-    return g_drv.cuMemHostGetFlags(&flags, const_cast<void *>(p)) == CUDA_SUCCESS;
+    CUpointer_attribute attr = CU_POINTER_ATTRIBUTE_MEMORY_TYPE;
+    unsigned type = 0;
+    void *data = &type;
+    return g_drv.cuPointerGetAttributes(1, &attr, &data, reinterpret_cast<CUdeviceptr>(p)) ==
+               CUDA_SUCCESS &&
+           type == CU_MEMORYTYPE_HOST;
 }
 
 struct CopyJob {
@@ -893,6 +902,13 @@ int rtcg_host_register(void *ptr, uint64_t nbytes) {
 int rtcg_host_unregister(void *ptr) {
     NEED_CONTEXT();
     CU_CALL(g_drv.cuMemHostUnregister(ptr), "cuMemHostUnregister");
+    return RTCG_OK;
+}
+
+int rtcg_host_is_pinned(const void *ptr, int *pinned) {
+    if (!pinned) return fail(RTCG_ERR_INVALID, "null output");
+    NEED_CONTEXT();
+    *pinned = is_pinned(ptr) ? 1 : 0;
     return RTCG_OK;
 }
 

@@ -112,6 +112,15 @@ def test_pinned_and_pageable_paths_agree(pool):
     out_pin = nd.pinned_empty((n,), nd.int64)
     a.to_host(out=out_pin)
     assert np.array_equal(out_pin, h) and np.array_equal(b.get(), h)
+    # an interior slice of a page-locked buffer is page-locked too (the
+    # runtime asks cuPointerGetAttributes for the memory type of the range)
+    assert _runtime.host_is_pinned(pin.ctypes.data)
+    assert _runtime.host_is_pinned(pin[7:].ctypes.data)
+    assert not _runtime.host_is_pinned(h.ctypes.data)
+    c = nd.from_host(pool, nd.int64, pin[7:])
+    out_view = out_pin[5:n - 2]
+    c.to_host(out=out_view)
+    assert np.array_equal(out_pin[5:n - 2], h[7:])
 
 
 def test_roofline_helper_reports_hbm_fraction(pool):
