@@ -13,6 +13,7 @@
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -39,6 +40,7 @@ struct Entry {
     long long resident = 1;    // SMs x occupancy (CTAs)
     int waves = 0;
     unsigned smem = 0;
+    long long min_parts = 0;   // partials a launch may store (dynamic chunks), beyond the grid
 };
 
 struct Plan {
@@ -60,12 +62,13 @@ void plan_dealloc(Plan *self) {
 }
 
 bool read_entry(PyObject *t, Entry &e) {
-    // (function, per_thread, resident, waves, smem)
+    // (function, per_thread, resident, waves, smem[, min_parts])
     unsigned long long fn;
-    long long pt, res;
+    long long pt, res, min_parts = 0;
     int waves;
     unsigned smem;
-    if (!PyArg_ParseTuple(t, "KLLiI", &fn, &pt, &res, &waves, &smem)) return false;
+    if (!PyArg_ParseTuple(t, "KLLiI|L", &fn, &pt, &res, &waves, &smem, &min_parts)) return false;
+    e.min_parts = min_parts > 0 ? min_parts : 0;
     e.fn = reinterpret_cast<void *>(fn);
     e.per_thread = pt > 0 ? pt : 1;
     e.resident = res > 0 ? res : 1;
@@ -257,7 +260,7 @@ PyObject *plan_launch(Plan *self, PyObject *const *argv, Py_ssize_t argc) {
     if (!vec_ok && !self->has_gen) Py_RETURN_NONE;   // general entry not built yet
     const Entry &e = vec_ok ? self->vec : self->gen;
     const long long grid = grid_of(self, e, n);
-    if (max_grid >= 0 && grid > max_grid) Py_RETURN_NONE;
+    if (max_grid >= 0 && std::max(grid, e.min_parts) > max_grid) Py_RETURN_NONE;
     vals[count] = static_cast<uint64_t>(base);
     vals[count + 1] = static_cast<uint64_t>(base + n);
     if (self->nextra) {

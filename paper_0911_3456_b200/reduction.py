@@ -42,9 +42,9 @@ from . import _codegen as cg
 from . import jit
 from . import ndarray as nd
 from .driver import HostArg as _HostArg, In as _In, InOut as _InOut, Out as _Out
-from .elementwise import (_CHUNK_TOKEN, _ERRORS, ArityMismatch, DtypeMismatch, KernelSignature,
-                          ParseError, VariantParams, _check_name, _LazyEntry, _preamble_text,
-                          parse_signature)
+from .elementwise import (_CHUNK_TOKEN, _ERRORS, MAX_CHUNKS, ArityMismatch, DtypeMismatch,
+                          KernelSignature, ParseError, VariantParams, _check_name, _LazyEntry,
+                          _preamble_text, parse_signature)
 from .ndarray import Dtype
 
 _HOST_CLASSES = frozenset({_HostArg, _In, _Out, _InOut})
@@ -125,7 +125,9 @@ def generate_reduction_source(spec: ReductionSpec, name: str,
     b.update(general=entries != "vector", combine=entries != "general")
     b["map_tparams"] = b.pop("op_tparams")
     b["map_params"] = b.pop("op_params")
+    dynamic = bool(variant.chunk) and b["vector"]
     b.update(name=name, unroll=variant.unroll, block=variant.block,
+             dynamic=dynamic, static=not dynamic, chunk=variant.chunk, max_chunks=MAX_CHUNKS,
              prefetch=variant.prefetch, no_prefetch=not variant.prefetch,
              preamble=_preamble_text(preamble), chunking=_CHUNK_TOKEN[variant.chunking],
              acc_t=spec.acc_dtype.cname, out_t=spec.out_dtype.cname,
@@ -325,6 +327,10 @@ class ReductionKernel:
         self._acc_ctype = nd.ctype_for(spec.acc_dtype)
         self._binder = cg.Binder(sig, extra=7)
         self._waves = 1 if self.variant.waves is None else self.variant.waves
+        # dynamic chunks: the vector entry stores up to MAX_CHUNKS partials
+        # (rtcg::chunk_plan grows the chunks to fit), whatever its grid
+        self._min_parts = MAX_CHUNKS if self.variant.chunk and self.vectorized is not None \
+            and not self.smem else 0
         self._scratch: dict[int, _Scratch] = {}
         self._lock = threading.Lock()
         self.launches = 0
@@ -418,7 +424,7 @@ class ReductionKernel:
             else:
                 per = self.variant.unroll * self.width
             vec = (fn, per, sms * max(1, _runtime.occupancy(fn, block, self.smem)), self._waves,
-                   self.smem)
+                   self.smem, self._min_parts)
         params = []
         for p in self.spec.signature.params:
             acc = self.access[p.name] if self.access is not None and p.is_vector else None
@@ -518,7 +524,7 @@ class ReductionKernel:
                 _runtime.set_max_dynamic_smem(fn, smem)
             grid = cg.grid_for(fn, dev, self.variant.block, self.variant.workers, n, per_thread,
                                self._waves, smem)
-        s.ensure(grid)
+        s.ensure(max(grid, self._min_parts if handle is self.vectorized else 0))
         rotate = overlap_previous and not _runtime.stream_is_capturing(stream)
         partials, seq = s.slot(rotate)
         if host_flag:

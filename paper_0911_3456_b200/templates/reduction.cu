@@ -135,8 +135,27 @@ ${name}(${kparams_vector}, const long start, const long end,
 ${unpack}
     constexpr int E = ${width};
     constexpr int U = ${unroll};
+{% if dynamic %}
+    // dynamic chunks (VariantParams.chunk, rtcg::chunk_plan): one partial
+    // per chunk, the next chunk id fetched while this one streams
+    const rtcg::chunks plan = rtcg::chunk_plan(start, end, ${chunk}L, ${max_chunks}L);
+    unsigned *const rtcg_ctr = rtcg::chunk_counter(rtcg_ticket, rtcg_seq);
+    __shared__ unsigned rtcg_next[2];
+    if (threadIdx.x == 0) rtcg_next[0] = atomicAdd(rtcg_ctr, 1u);
+    __syncthreads();
+    int rtcg_p = 0;
+    for (unsigned ch = rtcg_next[0]; ch < plan.count; ch = rtcg_next[rtcg_p]) {
+        if (threadIdx.x == 0) rtcg_next[rtcg_p ^ 1] = atomicAdd(rtcg_ctr, 1u);
+        rtcg::span sp;
+        sp.lo = max(start, plan.a0 + (long)ch * plan.size);
+        sp.hi = min(end, plan.a0 + ((long)ch + 1) * plan.size);
+        sp.first = threadIdx.x;
+        sp.step = blockDim.x;
+        ${acc_t} acc = ${neutral};
+{% endif %}{% if static %}
     ${acc_t} acc = ${neutral};
     const rtcg::span sp = rtcg::partition<rtcg::${chunking}>(start, end);
+{% endif %}
     const rtcg::tiles tl = rtcg::tile(sp.lo, sp.hi, E);
     auto elem = [&](const long i) {
         acc = rtcg_fold(acc, rtcg_map<${ptr_types_vector}>(i${call_args}));
@@ -186,8 +205,20 @@ ${vec_loads}
             }
         }
     }
+{% if dynamic %}
+        // the chunk's partial; block_fold's barriers also publish rtcg_next
+        acc = rtcg::block_fold(acc, RTCG_NEUTRAL,
+                               [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); });
+        if (threadIdx.x == 0) rtcg_partials[ch] = acc;
+        rtcg_p ^= 1;
+    }
+    rtcg::finish(RTCG_NEUTRAL, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
+                 [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch, rtcg_seq,
+                 plan.count);
+{% endif %}{% if static %}
     rtcg::finish(acc, RTCG_NEUTRAL, rtcg_partials, rtcg_result, rtcg_out, rtcg_ticket,
                  [](${acc_t} l, ${acc_t} r) { return rtcg_fold(l, r); }, rtcg_xr, rtcg_epoch, rtcg_seq);
+{% endif %}
 }
 {% endif %}
 {% if combine %}

@@ -19,7 +19,9 @@ _VARIANTS = (ew.VariantParams(), ew.VariantParams(unroll=1, block=64, workers=7)
              ew.VariantParams(unroll=8, block=512, chunking="contiguous-blocks"),
              ew.VariantParams(unroll=2, block=1024, workers=1),
              ew.VariantParams(cache="tma", block=256),
-             ew.VariantParams(cache="tma", block=64, workers=3))
+             ew.VariantParams(cache="tma", block=64, workers=3),
+             ew.VariantParams(unroll=4, block=256, chunk=8192),
+             ew.VariantParams(unroll=1, block=128, chunk=1024, workers=5))
 
 
 def test_reference_known_answers(kernel_env, golden):
@@ -394,3 +396,75 @@ def test_reduction_general_entry_is_compiled_on_first_need(kernel_env, tmp_path)
     assert k.generic.ready and jit.compiler_spawn_count() - before == 2
     assert int(k(x[1:])) == int(host[1:].sum())
     assert jit.compiler_spawn_count() - before == 2
+
+
+def test_dynamic_chunks_exact_and_deterministic(kernel_env):
+    """VariantParams.chunk (persistent CTAs taking chunks from a counter, one
+    partial per chunk folded in chunk order): integer sums bit-exact against
+    the C oracle at ragged sizes, base offsets and when the chunks must grow
+    (more than MAX_CHUNKS minimum-size chunks); float results identical for
+    every grid and call (the partials depend on the span, not on which CTA
+    took a chunk) and within the n*eps bound."""
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(77)
+    n_big = (ew.MAX_CHUNKS * 1024) + 4099           # chunk=1024 must grow to 2048
+    hi = rng.integers(-(1 << 62), 1 << 62, n_big, dtype=np.int64)
+    xi = nd.from_host(pool, nd.int64, hi)
+    oracle = cport.Reduction("int64_t *x", "int64", "0", "a + b", None, "sum_dyn")
+    for chunk, workers in ((1024, None), (8192, 3), (65536, 1)):
+        k = rd.sum_kernel(nd.int64, ew.VariantParams(chunk=chunk, workers=workers), **kwargs)
+        assert k.launch_config(xi)["entry"] == k.name          # the vector entry
+        for n in (1, 7, 1023, 1024, 1025, 3 * 8192 + 5, (1 << 20) + 3, n_big):
+            assert int(k(xi, n=n)) == int(oracle(hi, n=n)), (chunk, n)
+        # a span starting at an aligned global offset that is not a chunk multiple
+        o = pool.alloc_uninitialized(nd.int64, ())
+        base = 12348
+        k.launch(xi[base:], n=(1 << 20), base=base, out=o)
+        assert int(o.get()) == int(oracle(hi[base:], n=1 << 20))
+    hf = rng.uniform(-1, 1, n_big).astype(np.float32)
+    hg = rng.uniform(-1, 1, n_big).astype(np.float32)
+    xf, yf = nd.from_host(pool, nd.float32, hf), nd.from_host(pool, nd.float32, hg)
+    terms = (hf * hg).astype(np.float64)
+    exact, bound = csem.exact_sum(terms), csem.float_reduction_bound(terms, "float32")
+    results = set()
+    for workers in (None, 1, 7, 296):
+        k = rd.dot_kernel(nd.float32, ew.VariantParams(unroll=2, chunk=1024, workers=workers),
+                          **kwargs)
+        for _ in range(3):
+            got = float(k(xf, yf))
+            assert abs(got - exact) <= bound
+            results.add(got)
+    assert len(results) == 1
+
+
+def test_dynamic_chunks_overlapped_serial_and_captured(kernel_env):
+    """The chunk counters are per scratch slot and re-armed by the last CTA:
+    overlapped launches (alternating slots), serial launches and CUDA-graph
+    replays, interleaved on one scratch, each give the ordinary result."""
+    from paper_0911_3456_b200 import _runtime, graph
+    kwargs, pool = kernel_env
+    rng = np.random.default_rng(52)
+    n = 5_000_011
+    hx = rng.uniform(-1, 1, n).astype(np.float32)
+    hy = rng.uniform(-1, 1, n).astype(np.float32)
+    x, y = nd.from_host(pool, nd.float32, hx), nd.from_host(pool, nd.float32, hy)
+    dot = rd.dot_kernel(nd.float32, ew.VariantParams(unroll=4, chunk=4096), **kwargs)
+    want = float(dot(x, y))
+    outs = [pool.alloc_uninitialized(nd.float32, ()) for _ in range(60)]
+    for j in range(60):
+        dot.launch(x, y, out=outs[j], overlap_previous=j % 3 != 2)
+    assert [float(o.get()) for o in outs] == [want] * 60
+    st = _runtime.Stream()
+    with _runtime.use_stream(st.handle):
+        o = pool.alloc_uninitialized(nd.float32, ())
+        dot.launch(x, y, out=o)
+        st.synchronize()
+        g = graph.Graph(st)
+        with g.capture():
+            dot.launch(x, y, out=o, overlap_previous=True)
+        for _ in range(5):
+            g.launch()
+        st.synchronize()
+        assert float(o.get()) == want
+        g.close()
+    st.synchronize()

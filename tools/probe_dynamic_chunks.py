@@ -109,6 +109,32 @@ dyncta_dot(const float4 *__restrict__ x, const float4 *__restrict__ y, long n4, 
 }
 
 extern "C" __global__ void __launch_bounds__(256)
+dynpdl_dot(const float4 *__restrict__ x, const float4 *__restrict__ y, long n4, long ch4,
+           unsigned nch, double *partials, unsigned *ctrs, int launch)
+{
+    asm volatile("griddepcontrol.launch_dependents;");
+    unsigned *ctr = ctrs + launch;
+    double *part = partials + (long)(launch & 1) * nch;
+    __shared__ double red[32];
+    __shared__ unsigned next[2];
+    if (threadIdx.x == 0) next[0] = atomicAdd(ctr, 1u);
+    __syncthreads();
+    int p = 0;
+    unsigned ch = next[0];
+    while (ch < nch) {
+        if (threadIdx.x == 0) next[p ^ 1] = atomicAdd(ctr, 1u);
+        const long lo = (long)ch * ch4, hi = min(lo + ch4, n4);
+        double acc = 0.0;
+        for (long c = lo + threadIdx.x; c < hi; c += 4 * (long)blockDim.x)
+            acc = steps<4>(x, y, c, blockDim.x, hi, acc);
+        acc = block_sum(acc, red);
+        if (threadIdx.x == 0) part[ch] = acc;
+        p ^= 1;
+        ch = next[p];
+    }
+}
+
+extern "C" __global__ void __launch_bounds__(256)
 dynwarp_dot(const float4 *__restrict__ x, const float4 *__restrict__ y, long n4, long ch4,
             unsigned nch, double *partials, unsigned *ctr)
 {
@@ -134,7 +160,8 @@ dynwarp_dot(const float4 *__restrict__ x, const float4 *__restrict__ y, long n4,
 def main():
     rt.set_device(0)
     mod = jit.compile(SRC)
-    fns = {k: jit.get_kernel(mod, f"{k}_dot").function(0) for k in ("stat", "dyncta", "dynwarp")}
+    fns = {k: jit.get_kernel(mod, f"{k}_dot").function(0)
+           for k in ("stat", "dyncta", "dynwarp", "dynpdl")}
     n = 1 << 28
     n4 = n // 4
     x, y = rt.mem_alloc(n * 4), rt.mem_alloc(n * 4)
@@ -183,7 +210,7 @@ def main():
                      "burst_us": round(b * 1e3, 1), "burst_gbs": round(nbytes / (b * 1e-3) / 1e9, 1)}
 
     occ = rt.occupancy(fns["stat"], 256, 0)
-    for waves in (1, 2, 4):
+    for waves in (() if "--product-only" in sys.argv else (1, 2, 4)):
         grid = sms * occ * waves
         vals = [ctypes.c_uint64(x), ctypes.c_uint64(y), ctypes.c_int64(n4),
                 ctypes.c_uint64(partials), ctypes.c_uint64(stamps)]
@@ -197,10 +224,10 @@ def main():
             first_end_us=round(ends[0], 1), median_end_us=round(ends[len(ends) // 2], 1),
             p90_end_us=round(ends[int(0.9 * len(ends))], 1), last_end_us=round(ends[-1], 1))
         print(f"stat_waves{waves}", json.dumps(out[f"stat_waves{waves}"]), flush=True)
-    for kind in ("dyncta", "dynwarp"):
+    for kind in (() if "--product-only" in sys.argv else ("dyncta", "dynwarp")):
         occ_k = rt.occupancy(fns[kind], 256, 0)
-        chunks = (1 << 15, 1 << 16, 1 << 17, 1 << 18) if kind == "dyncta" else \
-            (1 << 12, 1 << 13, 1 << 14, 1 << 15)
+        chunks = (1 << 12, 1 << 13, 1 << 14, 1 << 15, 1 << 16, 1 << 18) if kind == "dyncta" \
+            else (1 << 12, 1 << 13, 1 << 14)
         for ch in chunks:
             ch4 = ch // 4
             nch = (n4 + ch4 - 1) // ch4
@@ -215,6 +242,33 @@ def main():
                 run(name, fns[kind], sms * rt.occupancy(fns[kind], 128, 0), vals, reset=True,
                     block=128)
                 print(name, json.dumps(out[name]), flush=True)
+    # dynamic chunks with programmatic dependent launch (per-launch counters,
+    # zeroed before the burst): the overlapped rate to compare with the
+    # product's burst_pdl_us
+    occ_p = rt.occupancy(fns["dynpdl"], 256, 0)
+    for ch in (() if "--product-only" in sys.argv else (1 << 13, 1 << 14)):
+        ch4 = ch // 4
+        nch = (n4 + ch4 - 1) // ch4
+        best = float("inf")
+        for _ in range(3):
+            rt.memset_async(ctrs, 0, 4 * 64)
+            rt.synchronize()
+            s_, e_ = rt.Event(), rt.Event()
+            s_.record()
+            for k in range(20):
+                vals = [ctypes.c_uint64(x), ctypes.c_uint64(y), ctypes.c_int64(n4),
+                        ctypes.c_int64(ch4), ctypes.c_uint32(nch), ctypes.c_uint64(partials),
+                        ctypes.c_uint64(ctrs), ctypes.c_int32(k)]
+                params = (ctypes.c_void_p * len(vals))(*[ctypes.addressof(v) for v in vals])
+                rt.launch_overlapped(fns["dynpdl"], sms * occ_p, 256, params)
+            e_.record()
+            e_.synchronize()
+            best = min(best, s_.elapsed_ms(e_) / 20)
+        name = f"dynpdl_chunk{ch}"
+        out[name] = {"grid": sms * occ_p, "burst_pdl_us": round(best * 1e3, 1),
+                     "burst_pdl_gbs": round(nbytes / (best * 1e-3) / 1e9, 1)}
+        print(name, json.dumps(out[name]), flush=True)
+
     # the product kernel on the same bytes (public API, isolated and overlapped)
     from paper_0911_3456_b200 import elementwise as ew, ndarray as nd, reduction as rd
     pool = nd.MemoryPool(device=0)
@@ -222,10 +276,14 @@ def main():
     rt.memset_async(gx.gpudata, 0x3c, n * 4)
     rt.memset_async(gy.gpudata, 0x3d, n * 4)
     o = pool.alloc(nd.float32, ())
-    for block, unroll, waves in ((128, 4, 2), (256, 4, 2), (512, 1, 2), (256, 4, 4)):
+    for block, unroll, waves, chunk in ((128, 4, 2, 0), (256, 4, 2, 0), (512, 1, 2, 0),
+                                        (1024, 1, 2, 0), (256, 4, 1, 8192), (256, 4, 1, 4096),
+                                        (256, 4, 1, 16384), (128, 4, 1, 8192),
+                                        (512, 1, 1, 8192), (256, 4, 2, 8192)):
         k = rd.ReductionKernel(rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b",
                                                 "x[i] * y[i]"), "dot_k",
-                               ew.VariantParams(block=block, unroll=unroll, waves=waves))
+                               ew.VariantParams(block=block, unroll=unroll, waves=waves,
+                                                chunk=chunk))
         for _ in range(3):
             k.launch(gx, gy, out=o)
         rt.synchronize()
@@ -248,7 +306,7 @@ def main():
             e.synchronize()
             res["pdl" if ov else "serial"] = s.elapsed_ms(e) / 20
         med = statistics.median(iso)
-        name = f"product_b{block}_u{unroll}_w{waves}"
+        name = f"product_b{block}_u{unroll}_w{waves}" + (f"_chunk{chunk}" if chunk else "")
         out[name] = {"isolated_us": round(med * 1e3, 1), "isolated_min_us": round(min(iso) * 1e3, 1),
                      "isolated_gbs": round(nbytes / (med * 1e-3) / 1e9, 1),
                      "burst_serial_us": round(res["serial"] * 1e3, 1),
