@@ -294,3 +294,24 @@ def test_overlapped_launches_with_the_peer_exchange(pool):
     assert all(float(o.get()) == float(want) for row in outs for o in row)
     for m in group:
         m.close()
+
+
+def test_emulated_ranks_with_dynamic_chunks(pool):
+    """VariantParams.chunk under the in-kernel exchange: each rank's chunk
+    partials fold in chunk order, then the ranks' accumulators in rank
+    order -- every rank ends with the ordered fold of the local results,
+    over four epochs (the chunk counters re-armed between them)."""
+    from paper_0911_3456_b200 import elementwise as ew, ndarray as nd, reduction as rd
+    rng = np.random.default_rng(12)
+    n, world = 8_000_000, 4                       # shard starts stay 16-byte aligned
+    x = rng.uniform(-1, 1, n).astype(np.float32)
+    y = rng.uniform(-1, 1, n).astype(np.float32)
+    dot = rd.dot_kernel(nd.float32, ew.VariantParams(unroll=2, chunk=4096))
+    shards = _shard(pool, nd.float32, [x, y], world)
+    assert dot.launch_config(*shards[1][0])["entry"] == dot.name     # the vector entry
+    want = par.ordered_fold(lambda a, b: a + b, 0.0, _rank_accumulators(dot, shards))
+    group = par.PeerMailbox.local_group(world)
+    for row in _emulate(dot, shards, group, rounds=4):
+        assert all(float(v) == float(want) for v in row), (row, want)
+    for m in group:
+        m.close()
