@@ -204,6 +204,16 @@ def test_axes_are_validated():
     with pytest.raises(ValueError):
         at._check_axes({"threads": (1,)})
     assert at._check_axes(None) == at.DEFAULT_AXES
+    # every VariantParams field is a tunable axis, dynamic chunks included
+    assert at._check_axes({"chunk": (0, 8192), "waves": (1,)})["chunk"] == (0, 8192)
+    from paper_0911_3456_b200 import elementwise as ew
+    with pytest.raises(ValueError):
+        ew.VariantParams(chunk=1000)                   # not a candidate size
+    with pytest.raises(ValueError):
+        ew.VariantParams(chunk=8192, cache="tma")      # the LDG vector path only
+    sig = ew.parse_signature("float *x, float *z")
+    with pytest.raises(ValueError):                    # reductions only
+        ew.generate(sig, "z[i] = x[i]", "k", ew.VariantParams(chunk=8192))
 
 
 # --- real kernels on the GPU -------------------------------------------------------------------
