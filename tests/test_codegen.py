@@ -205,6 +205,20 @@ def test_dot_reduction_compiles_with_fp64_accumulator(nvrtc_cache, tmp_path):
     assert "LDL" not in body and "STL" not in body  # no local-memory spills
 
 
+def test_dynamic_chunk_reduction_takes_chunks_from_a_counter(nvrtc_cache, tmp_path):
+    """VariantParams.chunk: the vector entry streams 128-bit chunks, takes
+    chunk ids with a global atomic, and still spills nothing."""
+    spec = rd.ReductionSpec("float *x, float *y", nd.float32, "0", "a + b", "x[i] * y[i]")
+    src = rd.generate_reduction_source(spec, "dot_k", ew.VariantParams(unroll=4, chunk=8192))
+    assert "rtcg::chunk_plan(start, end, 8192L" in src
+    static = rd.generate_reduction_source(spec, "dot_k", ew.VariantParams(unroll=4))
+    assert "chunk_plan" not in static.split("// ---- end prelude")[1]
+    sass = _sass(jit.compile(src, cache=nvrtc_cache).image, tmp_path)
+    body = sass.split("Function : dot_k\n")[1].split("Function :")[0]
+    assert "LDG.E.128" in body and "ATOMG.E.ADD" in body and "DADD" in body
+    assert "LDL" not in body and "STL" not in body
+
+
 @pytest.mark.parametrize("sig, op", [
     ("int8_t *b, double *d, double *z", "z[i] = b[i] * d[i] + 0.5"),
     ("uint64_t s, uint16_t *x, uint64_t *z", "z[i] = x[i] * s"),
