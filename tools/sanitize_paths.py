@@ -145,5 +145,25 @@ want = np.sin(trig_x[:5001]) + np.cos(trig_x[:5001])
 assert np.allclose(tz.get()[:5001], want, rtol=0, atol=1e-14)
 rd.make_reduction("double *x", nd.float64, "0", "a + b", "sin(x[i])", "sum_sin")(tx[:5001])
 checks += 1
+# dynamic chunk scheduling (VariantParams.chunk): tiny / ragged spans, a
+# base offset, overlapped launches alternating the slots' counters
+for n in (1, 4099, 100_003, 1 << 20):
+    hx = rng.uniform(-1, 1, n).astype(np.float32)
+    gx = nd.from_host(pool, nd.float32, hx)
+    for dv in (ew.VariantParams(chunk=1024), ew.VariantParams(unroll=4, block=128, chunk=4096,
+                                                              workers=3)):
+        dk = rd.dot_kernel(nd.float32, dv)
+        want = float(dk(gx, gx))
+        od = pool.alloc_uninitialized(nd.float32, ())
+        for _ in range(3):
+            dk.launch(gx, gx, out=od, overlap_previous=True)
+        assert float(od.get()) == want
+        checks += 4
+xi = nd.from_host(pool, nd.int64, rng.integers(-(1 << 40), 1 << 40, 300_000, dtype=np.int64))
+oi = pool.alloc_uninitialized(nd.int64, ())
+rd.sum_kernel(nd.int64, ew.VariantParams(chunk=2048)).launch(xi[4096:], n=200_000, base=4096,
+                                                              out=oi)
+assert int(oi.get()) == int(xi.get()[4096:204_096].sum())
+checks += 1
 rt.synchronize()
 print(f"sanitize paths ok ({checks} launches checked)")
