@@ -282,6 +282,12 @@ def test_template_locals_never_clash_with_user_names(nvrtc_cache, cache):
     spec = rd.ReductionSpec("float *b, long G, float *t", nd.float64, "0", "a + b",
                             "b[i] * t[i] + G")
     jit.compile(rd.generate_reduction_source(spec, "clash_r", v), cache=nvrtc_cache)
+    if cache != "tma":     # the dynamic-chunk locals (plan, ch, sp, tl) stay out of user scope
+        dyn = rd.ReductionSpec("float *x, long plan, double ch, int sp, int tl", nd.float32,
+                               "0", "a + b", "x[i] * plan + ch + sp + tl")
+        jit.compile(rd.generate_reduction_source(dyn, "clash_d",
+                                                 ew.VariantParams(unroll=2, chunk=4096)),
+                    cache=nvrtc_cache)
 
 
 def test_peer_descriptor_layout_matches_prelude(nvrtc_cache):
