@@ -31,6 +31,9 @@ def test_reference_arm_line():
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     cb = line["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and "sample" in cb
+    # the unmodified reference is preferred wherever it is installed
+    if (ROOT / "baseline" / "_ref" / "rtcg" / "reduction.py").exists():
+        assert "stock rtcg" in cb["sample"] and "baseline/_ref" in cb["sample"]
 
 
 @pytest.mark.gpu
